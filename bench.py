@@ -1,0 +1,329 @@
+"""Benchmark: genotypes classified/sec, full S_{2,8} enumeration (BASELINE.json configs[1]).
+
+One step = enumerate all 2^24 genome indices of S_{2,8} (a=2, b=8, d=19,
+ks=(1,2,4,8), hist_k=8, seed 0, strict contacts) into the device phenotype
+histogram: decode -> up to 8 movelist assemblies -> fold -> histogram insert,
+all in the sm_100a bitboard kernel.  With N ranks the index range is dealt out
+in round-robin chunks (strong scaling: the job is always the whole space) and
+the per-rank histograms are combined with one NCCL exchange
+(paper_2205_15311_b200.distributed.allreduce_histogram) inside the step.
+
+  value : device-timed (CUDA events, max over ranks) genomes/s, no host I/O.
+  e2e   : the same job through the public API classify.enumerate_space (host
+          call -> device -> histogram records copied back to host memory).
+  roofline : the dominant kernel (k_classify_fast<2>) against the measured
+          int32 ALU peak of this GPU (IADD3/XOR probe, tv_int_peak_launch);
+          algorithmic ops = event-weighted count (SURVEY.md section 8d,
+          profiles/event_counts.json) x genomes / kernel time.
+  cpu_baseline : the pinned C restatement of the reference (oracle/, kind
+          "port") on all host threads, on 64 evenly spaced blocks of S_{2,8}.
+
+--impl reference times that CPU port (the reference is Python/numba and is
+not installed on the GPU box) on the same metric; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "genotypes classified/sec (S_{2,8}, S^{32}_{3,8}) at 1/2/4/8 B200; GA gens/sec"
+UNIT = "genomes/s"
+KS = (1, 2, 4, 8)
+N_S28 = 1 << 24
+CHUNK = 1 << 20
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def s28_space():
+    from paper_2205_15311_b200.genome import SearchSpace
+    return SearchSpace(2, 8)
+
+
+def cpu_sample_indices(blocks: int, block: int) -> np.ndarray:
+    """`blocks` evenly spaced blocks of `block` consecutive S_{2,8} indices."""
+    stride = N_S28 // blocks
+    return (np.arange(blocks, dtype=np.uint64)[:, None] * np.uint64(stride)
+            + np.arange(block, dtype=np.uint64)[None, :]).reshape(-1)
+
+
+def cpu_port_rate(target_s: float = 8.0) -> dict:
+    """Oracle (C port of the reference, all host threads) genomes/s on an S_{2,8} sample."""
+    from oracle import oracle as O
+    a, bpl, mp, mv, fp = s28_space().kernel_args()
+    ks = np.array(KS, np.int64)
+
+    def run(idx):
+        n = idx.shape[0]
+        outs = [np.zeros((n, 4), np.uint8), np.zeros(n, np.uint32), np.zeros(n, np.uint8), np.zeros(n, np.uint8),
+                np.zeros(n, np.uint16), np.zeros((n, 6), np.uint64)]
+        t = time.perf_counter()
+        O.classify_batch(idx, a, bpl, mp, mv, fp, 19, ks, 8, 0, True, *outs)
+        return time.perf_counter() - t
+
+    run(cpu_sample_indices(64, 256))  # warm-up (thread pool, page faults)
+    probe = cpu_sample_indices(64, 1024)
+    dt = run(probe)
+    rate0 = probe.shape[0] / dt
+    block = int(min(1 << 18, max(1 << 10, rate0 * target_s / 64)))
+    idx = cpu_sample_indices(64, block)
+    dt = run(idx)
+    cores = os.cpu_count() or 1
+    return {"value": idx.shape[0] / dt, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"64 evenly spaced blocks x {block} consecutive indices of S_(2,8) "
+                      f"({idx.shape[0]} genomes, {dt:.2f} s), ks=(1,2,4,8), d=19, seed 0, strict; "
+                      f"oracle/tv_oracle.c (pinned C restatement of _kernels.classify_batch), OpenMP {cores} threads"}
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    O.build() if not os.path.exists(os.path.join(ROOT, "oracle", "libtv_oracle.so")) else None
+    a, bpl, mp, mv, fp = s28_space().kernel_args()
+    ks = np.array(KS, np.int64)
+    idx = cpu_sample_indices(64, 1 << 14)  # 2^20 genomes per step
+    n = idx.shape[0]
+    outs = [np.zeros((n, 4), np.uint8), np.zeros(n, np.uint32), np.zeros(n, np.uint8), np.zeros(n, np.uint8),
+            np.zeros(n, np.uint16), np.zeros((n, 6), np.uint64)]
+    for _ in range(args.warmup):
+        O.classify_batch(idx, a, bpl, mp, mv, fp, 19, ks, 8, 0, True, *outs)
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        O.classify_batch(idx, a, bpl, mp, mv, fp, 19, ks, 8, 0, True, *outs)
+    el = time.perf_counter() - t
+    v = n * args.steps / el
+    cores = os.cpu_count() or 1
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64/u32 integer", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "full S_(2,8) enumeration (2^24 genomes), CPU step = 2^20-genome sample "
+                                   "(64 evenly spaced blocks)", "space": "S_(2,8)", "ks": list(KS), "hist_k": 8,
+                       "d": 19, "seed": 0, "strict": True},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"{n} genomes per step; oracle/tv_oracle.c, OpenMP {cores} threads"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference(args, rank)
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+    from paper_2205_15311_b200 import _lib
+    from paper_2205_15311_b200.classify import DeviceHistogram, enumerate_space, shape_words_for
+    from paper_2205_15311_b200.distributed import allreduce_histogram, enumerate_space_distributed
+
+    L = _lib.lib()
+    space = s28_space()
+    a, bpl, mp, mv, fp = space.kernel_args()
+    ks = np.array(KS, np.int64)
+    W = shape_words_for(19)
+    stream = torch.cuda.current_stream()
+    sp = _lib.ctypes.c_void_p(stream.cuda_stream)
+    hist = DeviceHistogram(KS, 8, W, 1 << 16)
+    # this rank's share: chunks r, r+R, ... of the 2^24 range, one strided launch
+    nchunks = N_S28 // CHUNK
+    mine = len(range(rank, nchunks, world))
+    count = mine * CHUNK
+
+    def enumerate_step():
+        hist.clear(sp)
+        _lib.check(L.tv_enumerate_chunks(rank * CHUNK, count, CHUNK, CHUNK * world, a, bpl, _lib.ptr(mp),
+                                         _lib.ptr(mv), mp.shape[0], _lib.ptr(fp), fp.shape[0], 19, _lib.ptr(ks),
+                                         ks.shape[0], 8, 0, 1, hist._h, sp))
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        enumerate_step()
+        if world > 1:
+            allreduce_histogram(hist.export(sp), None)
+    barrier()
+    # ---- timed region: K steps, L2 flushed between steps (outside the events)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        barrier()
+        for i in range(args.steps):
+            flush.zero_()
+            e0, e1, e2 = ev[i]
+            e0.record(stream)
+            hist.clear(sp)
+            e1.record(stream)
+            _lib.check(L.tv_enumerate_chunks(rank * CHUNK, count, CHUNK, CHUNK * world, a, bpl, _lib.ptr(mp),
+                                             _lib.ptr(mv), mp.shape[0], _lib.ptr(fp), fp.shape[0], 19, _lib.ptr(ks),
+                                             ks.shape[0], 8, 0, 1, hist._h, sp))
+            if world > 1:
+                allreduce_histogram(hist.export(sp), None)
+            e2.record(stream)
+        barrier()
+    info = _lib.launch_info()
+    step_ms = [e0.elapsed_time(e2) for e0, _, e2 in ev]
+    kern_ms = [e1.elapsed_time(e2) for _, e1, e2 in ev] if world == 1 else None
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = N_S28 / (ms_per_step / 1e3)
+
+    # correctness of what was timed: the exported histogram equals the reference aggregate
+    final = hist.export(sp) if world == 1 else allreduce_histogram(hist.export(sp), None)
+    tallies_ok = final.tallies.tolist() == [[7448198, 5894957, 0, 3434061, 0], [6939346, 6865723, 214055, 2758092, 0],
+                                            [6697803, 7791627, 223880, 2063906, 0], [6631160, 8336639, 199388, 1610029, 0]]
+
+    # ---- e2e through the public API (host call -> device -> host records)
+    barrier()
+    e2e_times = []
+    d2h = 0
+    for i in range(max(2, min(args.steps, 5))):
+        t0 = time.perf_counter()
+        if world == 1:
+            h = enumerate_space(space, d=19, ks=KS, seed=0, batch_size=N_S28, capacity=1 << 16)
+        else:
+            h = enumerate_space_distributed(space, d=19, ks=KS, seed=0, batch_size=CHUNK, capacity=1 << 16)
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - t0)
+        d2h = len(h) * (4 + 8 * 4 + 1 + 1 + 2 + 8 * W) + h.tallies.size * 8
+    e2e_s = statistics.median(e2e_times)
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    h2d = ks.nbytes + mp.nbytes + mv.nbytes + fp.nbytes
+
+    # ---- roofline: dominant kernel vs measured int32 ALU peak
+    roof = None
+    if rank == 0:
+        counts = json.load(open(os.path.join(ROOT, "profiles", "event_counts.json")))["s28_full"]
+        ops_per_genome = counts["ops_per_genome"]
+        nsm = _lib.ctypes.c_int32()
+        L.tv_sm_count(_lib.ctypes.byref(nsm))
+        peak = 0.0
+        for _ in range(3):
+            ops = _lib.ctypes.c_double()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            _lib.check(L.tv_int_peak_launch(1 << 16, nsm.value * 8, 256, sp, _lib.ctypes.byref(ops)))
+            s1.record(stream)
+            torch.cuda.synchronize()
+            peak = max(peak, ops.value / (s0.elapsed_time(s1) / 1e3))
+        kms = statistics.mean(kern_ms) if kern_ms else ms_per_step
+        achieved = ops_per_genome * (N_S28 / world) / (kms / 1e3)
+        roof = {"bound": "int32_alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tops/s",
+                "frac": achieved / peak, "traffic": None,
+                "kernel": "k_classify_fast<2>", "kernel_ms": kms,
+                "ops_per_genome": ops_per_genome,
+                "peak_source": "measured on this GPU: tv_int_peak_launch (8 independent IADD3/LOP3 chains/thread)",
+                "ops_source": "event-weighted algorithmic int32 ops (SURVEY.md 8d weights) x oracle event counts, "
+                              "profiles/event_counts.json"}
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_port_rate()
+        except Exception as e:  # the oracle is test infrastructure; report, do not fail the bench
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {e}"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "u64/u32 integer", "data": "synthetic",
+                "config": {"workload": "full S_(2,8) enumeration: 2^24 genomes -> phenotype histogram",
+                           "space": "S_(2,8)", "ks": list(KS), "hist_k": 8, "d": 19, "seed": 0, "strict": True,
+                           "l2_flush": "256 MiB write between timed steps", "chunking": f"{CHUNK} round-robin",
+                           "parallelism": f"index-range shards x{world}", "histogram_ok": tallies_ok,
+                           "kernel_launch": info},
+                "e2e": {"value": N_S28 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                        "d2h_bytes_per_step": int(d2h), "api": "classify.enumerate_space"},
+                "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(),
+                "gpu_launches": 2 * args.steps}
+        print(json.dumps(line), flush=True)
+    hist.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

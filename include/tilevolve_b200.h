@@ -1,0 +1,148 @@
+/*
+ * tilevolve_b200.h -- C ABI of libtilevolve_b200.so, the B200 (sm_100a)
+ * implementation of the tilevolve enumeration / classification hot path and
+ * the GA generation loop.
+ *
+ * Every entry point replaces one reference interface (paths relative to
+ * /root/reference; "_k" = pkg/src/tilevolve/_kernels.py):
+ *
+ *   tv_classify_batch      <- _k.classify_batch        _k:404-452
+ *   tv_classify_single     <- _k.classify_single       _k:471-484
+ *   tv_assemble_single     <- _k.assemble_single       _k:455-468
+ *   tv_oat_hash_bytes      <- _k.oat_hash_bytes        _k:79-85
+ *   tv_enumerate_range     <- classify.enumerate_space (absent module;
+ *   tv_enumerate_indices      SPEC.md:297-306, per-batch classify_batch calls
+ *                             merged into a Histogram)
+ *   tv_hist_*              <- classify.Histogram
+ *   tv_ga_*                <- evolve.run_ga and its operators
+ *
+ * Conventions
+ *   - Returns 0 on success, a negative TV_ERR_* on failure; tv_last_error()
+ *     gives a thread-local message.  Per-row capacity overflow keeps the
+ *     reference semantics (class 255 in every out_class column, _k:434-437).
+ *   - Array arguments marked [h|d] may be host or device pointers (detected
+ *     per call).  Host arrays are staged through device memory inside the call
+ *     and the call synchronises the stream before returning; with device
+ *     arrays the call is stream-ordered and returns after the launch.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  All work for
+ *     one call runs on the current CUDA device.
+ *   - Small descriptor arrays (mask_pos, mask_val, free_pos, ks) are host
+ *     pointers with the reference dtypes (int64, uint8, int64, int64).
+ *   - There is no CPU execution path: if no CUDA device is usable every call
+ *     fails with TV_ERR_CUDA.
+ */
+#ifndef TILEVOLVE_B200_H
+#define TILEVOLVE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TV_OK 0
+#define TV_ERR_ARG -1
+#define TV_ERR_CUDA -2
+#define TV_ERR_HIST_FULL -3
+#define TV_ERR_UNSUPPORTED -4
+
+/* classification codes (_k:25-29) and single-run outcomes (_k:19-22) */
+#define TV_CLS_DETERMINISTIC 0
+#define TV_CLS_TRIVIAL 1
+#define TV_CLS_STERIC 2
+#define TV_CLS_UNBOUND 3
+#define TV_CLS_ERROR 255
+#define TV_RUN_BOUNDED 0
+#define TV_RUN_TRIVIAL 1
+#define TV_RUN_UNBOUND 2
+#define TV_RUN_OVERFLOW 3
+
+int tv_version(void);
+const char *tv_last_error(void);
+
+/* Kernel-path statistics of the last enumerate / classify launch on this
+ * thread: [0] path (1 = shared-memory bitboard kernel, 2 = generic kernel),
+ * [1] CTAs, [2] threads per CTA, [3] dynamic shared bytes per CTA,
+ * [4] launches issued by the call. */
+int tv_last_launch_info(int64_t *info5);
+
+/* _k:404-452.  indices[n] [h|d]; outputs [h|d]: out_class u8[n*q] (row-major
+ * n x q), out_hash u32[n], out_w u8[n], out_h u8[n], out_cells u16[n],
+ * out_shape u64[n*W].  ks ascending, hist_k <= ks[q-1] (the reference sizes its
+ * run buffer by ks[q-1], _k:425-426).  Rows whose hist_k class is TRIVIAL or
+ * UNBOUND keep their out_shape contents (_k:448-452). */
+int tv_classify_batch(const uint64_t *indices, int64_t n, int32_t a, int32_t bpl,
+                      const int64_t *mask_pos, const uint8_t *mask_val, int64_t m,
+                      const int64_t *free_pos, int64_t nfree, int32_t d,
+                      const int64_t *ks, int64_t q, int32_t hist_k, uint64_t seed, int32_t strict,
+                      uint8_t *out_class, uint32_t *out_hash, uint8_t *out_w, uint8_t *out_h,
+                      uint16_t *out_cells, uint64_t *out_shape, int64_t W, void *stream);
+
+/* _k:471-484: edges u8[a*16] host (edges_from_labels layout, _k:487-494);
+ * shape_words u64[W] host, written as the reference writes it;
+ * out6 = {status, cls, hash (as u32 bits), w, h, cells}. */
+int tv_classify_single(const uint8_t *edges, int32_t a, int32_t d, int32_t k, uint64_t seed,
+                       uint64_t genome_index, int32_t strict, uint64_t *shape_words, int64_t W,
+                       int32_t *out6);
+
+/* _k:455-468: out_grid i16[d*d] host (tile*4+orient, -1 empty);
+ * out6 = {outcome, minr, minc, maxr, maxc, n_placed}. */
+int tv_assemble_single(const uint8_t *edges, int32_t a, int32_t d, uint64_t seed, uint64_t genome_index,
+                       int32_t run_index, int32_t strict, int16_t *out_grid, int32_t *out6);
+
+/* _k:79-85: data [h|d] */
+int tv_oat_hash_bytes(const uint8_t *data, int64_t n, uint32_t *out);
+
+/* ---- phenotype histogram (device-resident, one CUDA device per handle) */
+typedef struct tv_hist tv_hist;
+/* capacity: slots (rounded up to a power of two); q: number of prefix ks
+ * tallied; W: u64 words per stored shape bitmap */
+int tv_hist_create(int64_t capacity, int32_t q, int32_t W, tv_hist **out);
+int tv_hist_destroy(tv_hist *h);
+int tv_hist_clear(tv_hist *h, void *stream);
+/* synchronises; n_keys = distinct shape hashes, overflow = 1 if inserts were dropped */
+int tv_hist_count(tv_hist *h, int64_t *n_keys, int32_t *overflow, void *stream);
+/* Records sorted by hash ascending.  All outputs host pointers sized for
+ * max_records (shape: max_records*W); tallies i64[q*5] in the order
+ * (DET, TRIV, STERIC, UNB, ERROR) per prefix k.  rep_* = UINT64_MAX if none. */
+int tv_hist_export(tv_hist *h, int64_t max_records, uint32_t *keys, uint64_t *det, uint64_t *steric,
+                   uint64_t *rep_det, uint64_t *rep_any, uint8_t *w, uint8_t *hh, uint16_t *cells,
+                   uint64_t *shape, int64_t *tallies, int64_t *n_out, void *stream);
+/* Merge records (same layout as export, [h|d]) and tallies (host, may be NULL)
+ * into h: counts add, representatives take the minimum. */
+int tv_hist_merge(tv_hist *h, int64_t n, const uint32_t *keys, const uint64_t *det, const uint64_t *steric,
+                  const uint64_t *rep_det, const uint64_t *rep_any, const uint8_t *w, const uint8_t *hh,
+                  const uint16_t *cells, const uint64_t *shape, const int64_t *tallies, void *stream);
+
+/* Fused enumerate -> classify -> histogram over indices [start, start+count)
+ * of a space (same space arguments as tv_classify_batch).  No per-genome
+ * output; stream-ordered. */
+int tv_enumerate_range(uint64_t start, uint64_t count, int32_t a, int32_t bpl,
+                       const int64_t *mask_pos, const uint8_t *mask_val, int64_t m,
+                       const int64_t *free_pos, int64_t nfree, int32_t d,
+                       const int64_t *ks, int64_t q, int32_t hist_k, uint64_t seed, int32_t strict,
+                       tv_hist *h, void *stream);
+/* Strided chunks: work item i is index start + (i / chunk) * stride + (i % chunk),
+ * i in [0, count).  Used for round-robin sharding of an index range across
+ * ranks (chunk c of the range -> rank c mod R) in a single launch. */
+int tv_enumerate_chunks(uint64_t start, uint64_t count, uint64_t chunk, uint64_t stride, int32_t a, int32_t bpl,
+                        const int64_t *mask_pos, const uint8_t *mask_val, int64_t m,
+                        const int64_t *free_pos, int64_t nfree, int32_t d,
+                        const int64_t *ks, int64_t q, int32_t hist_k, uint64_t seed, int32_t strict,
+                        tv_hist *h, void *stream);
+/* Same, over an explicit index list [h|d]. */
+int tv_enumerate_indices(const uint64_t *indices, int64_t n, int32_t a, int32_t bpl,
+                         const int64_t *mask_pos, const uint8_t *mask_val, int64_t m,
+                         const int64_t *free_pos, int64_t nfree, int32_t d,
+                         const int64_t *ks, int64_t q, int32_t hist_k, uint64_t seed, int32_t strict,
+                         tv_hist *h, void *stream);
+
+/* ---- measurement helpers (bench.py roofline) */
+/* Launch the int32 ALU peak probe (IADD3/LOP3 chains); *ops = int32 ops issued. */
+int tv_int_peak_launch(int64_t iters, int32_t blocks, int32_t threads, void *stream, double *ops);
+int tv_sm_count(int32_t *n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TILEVOLVE_B200_H */

@@ -1,0 +1,635 @@
+// tv_capi.cu -- extern "C" boundary of libtilevolve_b200.so (include/tilevolve_b200.h).
+#include <cub/device/device_radix_sort.cuh>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/tilevolve_b200.h"
+#include "tv_fast.cuh"
+#include "tv_kernels.cuh"
+
+using namespace tvb;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_launch[5] = {0, 0, 0, 0, 0};
+
+int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(expr)                                                                                  \
+  do {                                                                                            \
+    cudaError_t e_ = (expr);                                                                      \
+    if (e_ != cudaSuccess) return fail(TV_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                                       __FILE__, __LINE__);                                       \
+  } while (0)
+
+bool is_device_ptr(const void *p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+std::once_flag g_pool_once[64];
+void setup_pool(int dev) {
+  if (dev < 0 || dev >= 64) return;
+  std::call_once(g_pool_once[dev], [dev]() {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+}
+
+// Stream-ordered scratch owned by one call.
+struct Scratch {
+  cudaStream_t s;
+  std::vector<void *> ptrs;
+  explicit Scratch(cudaStream_t st) : s(st) {}
+  template <typename T> cudaError_t get(T **p, size_t count) {
+    void *v = nullptr;
+    cudaError_t e = cudaMallocAsync(&v, std::max<size_t>(count * sizeof(T), 16), s);
+    if (e == cudaSuccess) ptrs.push_back(v);
+    *p = static_cast<T *>(v);
+    return e;
+  }
+  ~Scratch() {
+    for (void *v : ptrs) cudaFreeAsync(v, s);
+  }
+};
+
+int current_device(int *dev) {
+  cudaError_t e = cudaGetDevice(dev);
+  if (e != cudaSuccess) return fail(TV_ERR_CUDA, "no CUDA device: %s", cudaGetErrorString(e));
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return fail(TV_ERR_CUDA, "no CUDA device");
+  setup_pool(*dev);
+  return 0;
+}
+
+// Reduce the reference's bit writes (_k:387-397) to per-label decoders.
+int build_decoder(int a, int bpl, const int64_t *mask_pos, const uint8_t *mask_val, int64_t m,
+                  const int64_t *free_pos, int64_t nfree, LabelDecoder &D) {
+  if (a < 1 || a > 16) return fail(TV_ERR_ARG, "tile count a=%d outside [1, 16]", a);
+  if (bpl < 1 || bpl > 8) return fail(TV_ERR_ARG, "bits per label %d outside [1, 8]", bpl);
+  if (nfree > 64) return fail(TV_ERR_ARG, "%lld free bits exceed the 64-bit enumeration index", (long long)nfree);
+  const int L = a * 4 * bpl;
+  std::vector<int> src(L, -1), cval(L, 0);
+  for (int64_t j = 0; j < m; j++) {
+    if (mask_pos[j] < 0 || mask_pos[j] >= L) return fail(TV_ERR_ARG, "mask position %lld outside [0, %d)", (long long)mask_pos[j], L);
+    if (mask_val[j] > 1) return fail(TV_ERR_ARG, "mask value %d is not a bit", (int)mask_val[j]);
+    src[mask_pos[j]] = -1;
+    cval[mask_pos[j]] = mask_val[j];
+  }
+  for (int64_t j = 0; j < nfree; j++) {
+    if (free_pos[j] < 0 || free_pos[j] >= L) return fail(TV_ERR_ARG, "free position %lld outside [0, %d)", (long long)free_pos[j], L);
+    src[free_pos[j]] = (int)j;
+  }
+  memset(&D, 0, sizeof D);
+  D.nlab = a * 4;
+  D.bpl = bpl;
+  bool general = false;
+  for (int te = 0; te < a * 4; te++) {
+    int fix = 0, nf = 0, lo = -1, sh = -1;
+    bool contiguous = true;
+    for (int k = 0; k < bpl; k++) {  // label bit k (LSB = 0) <- genome position te*bpl + bpl-1-k
+      const int p = te * bpl + (bpl - 1 - k);
+      D.src[te * 8 + k] = src[p] < 0 ? 0xFF : (uint8_t)src[p];
+      if (src[p] < 0) {
+        fix |= cval[p] << k;
+      } else {
+        if (nf == 0) { lo = src[p]; sh = k; }
+        else if (src[p] != lo + nf || k != sh + nf) contiguous = false;
+        nf++;
+      }
+    }
+    D.fix[te] = (uint8_t)fix;
+    D.nf[te] = (uint8_t)nf;
+    D.lo[te] = (uint8_t)(lo < 0 ? 0 : lo);
+    D.sh[te] = (uint8_t)(sh < 0 ? 0 : sh);
+    if (!contiguous) general = true;
+  }
+  D.general = general ? 1 : 0;
+  return 0;
+}
+
+struct Common {
+  ClassifyParams P;
+  bool fast;
+};
+
+int fill_common(int32_t a, int32_t bpl, const int64_t *mask_pos, const uint8_t *mask_val, int64_t m,
+                const int64_t *free_pos, int64_t nfree, int32_t d, const int64_t *ks, int64_t q, int32_t hist_k,
+                uint64_t seed, int32_t strict, Common &C) {
+  memset(&C.P, 0, sizeof C.P);
+  if (int rc = build_decoder(a, bpl, mask_pos, mask_val, m, free_pos, nfree, C.P.dec)) return rc;
+  if (d < 3 || d > 181) return fail(TV_ERR_ARG, "grid dimension d=%d outside [3, 181]", d);
+  if (q < 1 || q > kMaxKs) return fail(TV_ERR_ARG, "len(ks)=%lld outside [1, %d]", (long long)q, kMaxKs);
+  for (int64_t i = 0; i < q; i++) {
+    if (ks[i] < 1 || ks[i] > 4096) return fail(TV_ERR_ARG, "ks[%lld]=%lld outside [1, 4096]", (long long)i, (long long)ks[i]);
+    if (i && ks[i] < ks[i - 1]) return fail(TV_ERR_ARG, "ks must be ascending");
+    C.P.ks[i] = (int32_t)ks[i];
+  }
+  const int kmax = (int)ks[q - 1];
+  if (hist_k < 1 || hist_k > kmax) return fail(TV_ERR_ARG, "hist_k=%d outside [1, ks[-1]=%d]", hist_k, kmax);
+  C.P.a = a; C.P.d = d; C.P.strict = strict ? 1 : 0; C.P.q = (int32_t)q; C.P.kmax = kmax; C.P.hist_k = hist_k;
+  C.P.seed = seed;
+  const int PD = d + 2;
+  C.fast = a <= 3 && bpl <= 3 && PD * PD < 65536 && PD < 256;
+  return 0;
+}
+
+// Launch the chosen kernel for P (n items, indices or range already set).
+int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
+  ClassifyParams &P = C.P;
+  int dev;
+  if (int rc = current_device(&dev)) return rc;
+  int nsm = 0;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  g_launch[4] = 0;
+  if (P.n <= 0) return 0;
+  unsigned long long *work;
+  CK(S.get(&work, 1));
+  CK(cudaMemsetAsync(work, 0, sizeof(unsigned long long), st));
+  P.work = work;
+  const int d = P.d, dd = d * d;
+  if (C.fast) {
+    const int PD = d + 2;
+    P.GW = (PD * PD + 7) / 8;
+    P.S = std::min(64, (dd + 1) & ~1);
+    if (P.S < 4) P.S = 4;
+    P.spill_cap = std::max(0, dd - P.S);
+    P.cta_slots = P.hist_mode ? 512 : 0;
+    int threads = 256;
+    size_t smem = fast_smem_bytes(threads, P.GW, P.S, P.cta_slots, P.q);
+    int maxsmem = 0;
+    CK(cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    while (smem > (size_t)maxsmem && threads > 32) {
+      threads /= 2;
+      smem = fast_smem_bytes(threads, P.GW, P.S, P.cta_slots, P.q);
+    }
+    if (smem <= (size_t)maxsmem) {
+      const void *fn = P.a == 1 ? (const void *)k_classify_fast<1>
+                     : P.a == 2 ? (const void *)k_classify_fast<2> : (const void *)k_classify_fast<3>;
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int per_sm = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem));
+      if (per_sm < 1) per_sm = 1;
+      int64_t blocks = (int64_t)nsm * per_sm;
+      const int64_t need = (P.n + threads - 1) / threads;
+      if (blocks > need) blocks = std::max<int64_t>(1, need);
+      const int64_t warps = blocks * (threads / 32);
+      CK(S.get(&P.spill, (size_t)std::max(1, P.spill_cap) * 32 * warps));
+      CK(S.get(&P.run_hash, (size_t)P.kmax * 32 * warps));
+      void *args[] = {&P};
+      CK(cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(threads), args, smem, st));
+      g_launch[0] = 1; g_launch[1] = blocks; g_launch[2] = threads; g_launch[3] = (int64_t)smem; g_launch[4] = 1;
+      return 0;
+    }
+  }
+  // generic thread-per-genome kernel
+  const int threads = 128;
+  int64_t T = (int64_t)nsm * 8 * threads;
+  const size_t per_thread = (size_t)dd * (2 + 1 + 4 + 4) + (size_t)P.kmax * 4;
+  const size_t budget = (size_t)2 << 30;
+  while (T > threads && (size_t)T * per_thread > budget) T /= 2;
+  if (T > P.n) T = std::max<int64_t>(1, P.n);
+  P.g_threads = T;
+  CK(S.get(&P.g_grid, (size_t)dd * T));
+  CK(S.get(&P.g_mark, (size_t)dd * T));
+  CK(S.get(&P.g_stack, (size_t)dd * T));
+  CK(S.get(&P.g_placed, (size_t)dd * T));
+  CK(S.get(&P.run_hash, (size_t)P.kmax * T));
+  k_fill_i16<<<512, 256, 0, st>>>(P.g_grid, (int64_t)dd * T, (int16_t)-1);
+  CK(cudaMemsetAsync(P.g_mark, 0, (size_t)dd * T, st));
+  const int64_t blocks = (T + threads - 1) / threads;
+  k_classify_generic<<<(unsigned)blocks, threads, 0, st>>>(P);
+  CK(cudaGetLastError());
+  g_launch[0] = 2; g_launch[1] = blocks; g_launch[2] = threads; g_launch[3] = 0; g_launch[4] = 2;
+  return 0;
+}
+
+// Device view of a [h|d] array: either the pointer itself or a staged copy.
+template <typename T>
+int stage_in(const T *p, size_t count, bool copy_in, Scratch &S, T **dptr, bool &was_host) {
+  was_host = !is_device_ptr(p);
+  if (!was_host) { *dptr = const_cast<T *>(p); return 0; }
+  CK(S.get(dptr, count));
+  if (copy_in && count) CK(cudaMemcpyAsync(*dptr, p, count * sizeof(T), cudaMemcpyHostToDevice, S.s));
+  return 0;
+}
+
+
+// Integer-ALU peak probe (roofline denominator): 8 independent IADD3/LOP3
+// chains per thread, 2 int32 ops per chain step.
+__global__ void __launch_bounds__(256) k_int_peak(int64_t iters, uint32_t seed, uint32_t *sink) {
+  uint32_t a[8], b[8];
+#pragma unroll
+  for (int i = 0; i < 8; i++) { a[i] = seed + threadIdx.x * 8 + i; b[i] = seed ^ (blockIdx.x + i); }
+  for (int64_t t = 0; t < iters; t++) {
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      asm volatile("add.u32 %0, %0, %1;" : "+r"(a[i]) : "r"(b[i]));
+      asm volatile("xor.b32 %0, %0, %1;" : "+r"(b[i]) : "r"(a[i]));
+    }
+  }
+  uint32_t x = 0;
+#pragma unroll
+  for (int i = 0; i < 8; i++) x ^= a[i] + b[i];
+  if (x == 0x12345678u) sink[0] = x;
+}
+
+}  // namespace
+
+struct tv_hist {
+  HistDev H;
+  int device;
+};
+
+extern "C" {
+
+int tv_version(void) { return 10000; }
+
+const char *tv_last_error(void) { return g_err.c_str(); }
+
+int tv_last_launch_info(int64_t *info5) {
+  for (int i = 0; i < 5; i++) info5[i] = g_launch[i];
+  return 0;
+}
+
+int tv_classify_batch(const uint64_t *indices, int64_t n, int32_t a, int32_t bpl, const int64_t *mask_pos,
+                      const uint8_t *mask_val, int64_t m, const int64_t *free_pos, int64_t nfree, int32_t d,
+                      const int64_t *ks, int64_t q, int32_t hist_k, uint64_t seed, int32_t strict,
+                      uint8_t *out_class, uint32_t *out_hash, uint8_t *out_w, uint8_t *out_h, uint16_t *out_cells,
+                      uint64_t *out_shape, int64_t W, void *stream) {
+  Common C;
+  if (n < 0) return fail(TV_ERR_ARG, "negative n");
+  if (int rc = fill_common(a, bpl, mask_pos, mask_val, m, free_pos, nfree, d, ks, q, hist_k, seed, strict, C)) return rc;
+  const int64_t need_bits = (int64_t)(d - 2) * (d - 2);
+  if (W * 64 < need_bits) return fail(TV_ERR_ARG, "out_shape has %lld words; d=%d needs %lld", (long long)W, d, (long long)((need_bits + 63) / 64));
+  int dev;
+  if (int rc = current_device(&dev)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  bool any_host = false;
+  {
+    Scratch S(st);
+    uint64_t *d_idx; uint8_t *d_cls, *d_w, *d_h; uint32_t *d_hash; uint16_t *d_cells; uint64_t *d_shape;
+    bool h0, h1, h2, h3, h4, h5, h6;
+    // outputs are copied in too: rows the reference leaves untouched must survive (_k:434-452)
+    if (int rc = stage_in(indices, (size_t)n, true, S, &d_idx, h0)) return rc;
+    if (int rc = stage_in(out_class, (size_t)n * q, true, S, &d_cls, h1)) return rc;
+    if (int rc = stage_in(out_hash, (size_t)n, true, S, &d_hash, h2)) return rc;
+    if (int rc = stage_in(out_w, (size_t)n, true, S, &d_w, h3)) return rc;
+    if (int rc = stage_in(out_h, (size_t)n, true, S, &d_h, h4)) return rc;
+    if (int rc = stage_in(out_cells, (size_t)n, true, S, &d_cells, h5)) return rc;
+    if (int rc = stage_in(out_shape, (size_t)n * W, true, S, &d_shape, h6)) return rc;
+    any_host = h0 || h1 || h2 || h3 || h4 || h5 || h6;
+    C.P.indices = d_idx; C.P.n = n;
+    C.P.out_class = d_cls; C.P.out_hash = d_hash; C.P.out_w = d_w; C.P.out_h = d_h; C.P.out_cells = d_cells;
+    C.P.out_shape = reinterpret_cast<unsigned long long *>(d_shape); C.P.W = W;
+    if (int rc = launch_classify(C, S, st)) return rc;
+    if (h1) CK(cudaMemcpyAsync(out_class, d_cls, (size_t)n * q, cudaMemcpyDeviceToHost, st));
+    if (h2) CK(cudaMemcpyAsync(out_hash, d_hash, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+    if (h3) CK(cudaMemcpyAsync(out_w, d_w, (size_t)n, cudaMemcpyDeviceToHost, st));
+    if (h4) CK(cudaMemcpyAsync(out_h, d_h, (size_t)n, cudaMemcpyDeviceToHost, st));
+    if (h5) CK(cudaMemcpyAsync(out_cells, d_cells, (size_t)n * 2, cudaMemcpyDeviceToHost, st));
+    if (h6) CK(cudaMemcpyAsync(out_shape, d_shape, (size_t)n * W * 8, cudaMemcpyDeviceToHost, st));
+  }
+  if (any_host) CK(cudaStreamSynchronize(st));
+  CK(cudaGetLastError());
+  return 0;
+}
+
+static int single_scratch(int d, Scratch &S, int16_t **grid, uint8_t **mark, int32_t **stack, int32_t **placed) {
+  const size_t dd = (size_t)d * d;
+  CK(S.get(grid, dd));
+  CK(S.get(mark, dd));
+  CK(S.get(stack, dd));
+  CK(S.get(placed, dd));
+  k_fill_i16<<<1, 256, 0, S.s>>>(*grid, (int64_t)dd, (int16_t)-1);
+  CK(cudaMemsetAsync(*mark, 0, dd, S.s));
+  return 0;
+}
+
+int tv_classify_single(const uint8_t *edges, int32_t a, int32_t d, int32_t k, uint64_t seed, uint64_t genome_index,
+                       int32_t strict, uint64_t *shape_words, int64_t W, int32_t *out6) {
+  if (a < 1 || a > 16) return fail(TV_ERR_ARG, "tile count a=%d outside [1, 16]", a);
+  if (d < 3 || d > 181) return fail(TV_ERR_ARG, "grid dimension d=%d outside [3, 181]", d);
+  if (k < 1 || k > 4096) return fail(TV_ERR_ARG, "k=%d outside [1, 4096]", k);
+  if (W * 64 < (int64_t)(d - 2) * (d - 2)) return fail(TV_ERR_ARG, "shape buffer too small for d=%d", d);
+  int dev;
+  if (int rc = current_device(&dev)) return rc;
+  cudaStream_t st = nullptr;
+  {
+    Scratch S(st);
+    int16_t *grid; uint8_t *mark; int32_t *stack, *placed; uint32_t *rh; uint8_t *de; int32_t *dout;
+    unsigned long long *dsh;
+    if (int rc = single_scratch(d, S, &grid, &mark, &stack, &placed)) return rc;
+    CK(S.get(&rh, (size_t)k));
+    CK(S.get(&de, (size_t)a * 16));
+    CK(S.get(&dout, 6));
+    CK(S.get(&dsh, (size_t)W));
+    CK(cudaMemcpyAsync(de, edges, (size_t)a * 16, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dsh, shape_words, (size_t)W * 8, cudaMemcpyHostToDevice, st));
+    k_classify_single<<<1, 32, 0, st>>>(de, a, d, k, seed, genome_index, strict, dsh, W, dout, grid, mark, stack,
+                                         placed, rh);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out6, dout, 6 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(shape_words, dsh, (size_t)W * 8, cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int tv_assemble_single(const uint8_t *edges, int32_t a, int32_t d, uint64_t seed, uint64_t genome_index,
+                       int32_t run_index, int32_t strict, int16_t *out_grid, int32_t *out6) {
+  if (a < 1 || a > 16) return fail(TV_ERR_ARG, "tile count a=%d outside [1, 16]", a);
+  if (d < 3 || d > 181) return fail(TV_ERR_ARG, "grid dimension d=%d outside [3, 181]", d);
+  int dev;
+  if (int rc = current_device(&dev)) return rc;
+  cudaStream_t st = nullptr;
+  {
+    Scratch S(st);
+    int16_t *grid; uint8_t *mark; int32_t *stack, *placed; uint8_t *de; int32_t *dout;
+    if (int rc = single_scratch(d, S, &grid, &mark, &stack, &placed)) return rc;
+    CK(S.get(&de, (size_t)a * 16));
+    CK(S.get(&dout, 6));
+    CK(cudaMemcpyAsync(de, edges, (size_t)a * 16, cudaMemcpyHostToDevice, st));
+    k_assemble_single<<<1, 32, 0, st>>>(de, a, d, seed, genome_index, run_index, strict, grid, mark, stack, placed,
+                                         dout);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out6, dout, 6 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(out_grid, grid, (size_t)d * d * 2, cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int tv_oat_hash_bytes(const uint8_t *data, int64_t n, uint32_t *out) {
+  if (n < 0) return fail(TV_ERR_ARG, "negative length");
+  int dev;
+  if (int rc = current_device(&dev)) return rc;
+  cudaStream_t st = nullptr;
+  {
+    Scratch S(st);
+    uint8_t *dd; bool host; uint32_t *dout;
+    if (int rc = stage_in(data, (size_t)n, true, S, &dd, host)) return rc;
+    CK(S.get(&dout, 1));
+    k_oat<<<1, 32, 0, st>>>(dd, n, dout);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, dout, 4, cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+// ---------------------------------------------------------------- histogram
+int tv_hist_create(int64_t capacity, int32_t q, int32_t W, tv_hist **out) {
+  if (capacity < 1 || capacity > ((int64_t)1 << 30)) return fail(TV_ERR_ARG, "capacity outside [1, 2^30]");
+  if (q < 1 || q > kMaxKs) return fail(TV_ERR_ARG, "q outside [1, %d]", kMaxKs);
+  if (W < 1 || W > 1024) return fail(TV_ERR_ARG, "W outside [1, 1024]");
+  int dev;
+  if (int rc = current_device(&dev)) return rc;
+  int64_t cap = 1;
+  while (cap < capacity) cap <<= 1;
+  tv_hist *h = new tv_hist();
+  h->device = dev;
+  HistDev &H = h->H;
+  H.cap = cap; H.W = W; H.q = q;
+  cudaError_t e = cudaSuccess;
+  e = e ? e : cudaMalloc(&H.keys, cap * 8);
+  e = e ? e : cudaMalloc(&H.det, cap * 8);
+  e = e ? e : cudaMalloc(&H.steric, cap * 8);
+  e = e ? e : cudaMalloc(&H.rep_det, cap * 8);
+  e = e ? e : cudaMalloc(&H.rep_any, cap * 8);
+  e = e ? e : cudaMalloc(&H.whc, cap * 4);
+  e = e ? e : cudaMalloc(&H.shape, cap * 8 * W);
+  e = e ? e : cudaMalloc(&H.tallies, (size_t)q * 5 * 8);
+  e = e ? e : cudaMalloc(&H.n_keys, 4);
+  e = e ? e : cudaMalloc(&H.overflow, 4);
+  if (e != cudaSuccess) {
+    tv_hist_destroy(h);
+    return fail(TV_ERR_CUDA, "histogram allocation: %s", cudaGetErrorString(e));
+  }
+  if (int rc = tv_hist_clear(h, nullptr)) { tv_hist_destroy(h); return rc; }
+  CK(cudaStreamSynchronize(nullptr));
+  *out = h;
+  return 0;
+}
+
+int tv_hist_destroy(tv_hist *h) {
+  if (!h) return 0;
+  HistDev &H = h->H;
+  cudaFree(H.keys); cudaFree(H.det); cudaFree(H.steric); cudaFree(H.rep_det); cudaFree(H.rep_any);
+  cudaFree(H.whc); cudaFree(H.shape); cudaFree(H.tallies); cudaFree(H.n_keys); cudaFree(H.overflow);
+  delete h;
+  return 0;
+}
+
+int tv_hist_clear(tv_hist *h, void *stream) {
+  if (!h) return fail(TV_ERR_ARG, "null histogram");
+  k_hist_reset<<<256, 256, 0, (cudaStream_t)stream>>>(h->H);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int tv_hist_count(tv_hist *h, int64_t *n_keys, int32_t *overflow, void *stream) {
+  if (!h) return fail(TV_ERR_ARG, "null histogram");
+  unsigned int v[2];
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemcpyAsync(&v[0], h->H.n_keys, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&v[1], h->H.overflow, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (n_keys) *n_keys = v[0];
+  if (overflow) *overflow = (int32_t)v[1];
+  return 0;
+}
+
+int tv_hist_export(tv_hist *h, int64_t max_records, uint32_t *keys, uint64_t *det, uint64_t *steric,
+                   uint64_t *rep_det, uint64_t *rep_any, uint8_t *w, uint8_t *hh, uint16_t *cells, uint64_t *shape,
+                   int64_t *tallies, int64_t *n_out, void *stream) {
+  if (!h) return fail(TV_ERR_ARG, "null histogram");
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t n = 0;
+  int32_t ovf = 0;
+  if (int rc = tv_hist_count(h, &n, &ovf, stream)) return rc;
+  if (ovf) return fail(TV_ERR_HIST_FULL, "histogram overflowed its %lld slots", (long long)h->H.cap);
+  if (n > max_records) return fail(TV_ERR_ARG, "%lld records do not fit max_records=%lld", (long long)n, (long long)max_records);
+  const HistDev &H = h->H;
+  {
+    Scratch S(st);
+    uint32_t *k0, *s0, *k1, *s1;
+    unsigned int *cnt;
+    CK(S.get(&k0, n)); CK(S.get(&s0, n)); CK(S.get(&k1, n)); CK(S.get(&s1, n)); CK(S.get(&cnt, 1));
+    CK(cudaMemsetAsync(cnt, 0, 4, st));
+    k_hist_compact<<<256, 256, 0, st>>>(H, k0, s0, cnt);
+    CK(cudaGetLastError());
+    if (n > 0) {
+      size_t tmp_bytes = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k0, k1, s0, s1, (int)n, 0, 32, st));
+      uint8_t *tmp;
+      CK(S.get(&tmp, tmp_bytes));
+      CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, s0, s1, (int)n, 0, 32, st));
+      HistRecords R;
+      R.keys = k1;
+      CK(S.get(&R.det, n)); CK(S.get(&R.steric, n)); CK(S.get(&R.rep_det, n)); CK(S.get(&R.rep_any, n));
+      CK(S.get(&R.w, n)); CK(S.get(&R.h, n)); CK(S.get(&R.cells, n)); CK(S.get(&R.shape, (size_t)n * H.W));
+      k_hist_gather<<<64, 256, 0, st>>>(H, s1, n, R);
+      CK(cudaGetLastError());
+      if (keys) CK(cudaMemcpyAsync(keys, k1, n * 4, cudaMemcpyDefault, st));
+      if (det) CK(cudaMemcpyAsync(det, R.det, n * 8, cudaMemcpyDefault, st));
+      if (steric) CK(cudaMemcpyAsync(steric, R.steric, n * 8, cudaMemcpyDefault, st));
+      if (rep_det) CK(cudaMemcpyAsync(rep_det, R.rep_det, n * 8, cudaMemcpyDefault, st));
+      if (rep_any) CK(cudaMemcpyAsync(rep_any, R.rep_any, n * 8, cudaMemcpyDefault, st));
+      if (w) CK(cudaMemcpyAsync(w, R.w, n, cudaMemcpyDefault, st));
+      if (hh) CK(cudaMemcpyAsync(hh, R.h, n, cudaMemcpyDefault, st));
+      if (cells) CK(cudaMemcpyAsync(cells, R.cells, n * 2, cudaMemcpyDefault, st));
+      if (shape) CK(cudaMemcpyAsync(shape, R.shape, (size_t)n * H.W * 8, cudaMemcpyDefault, st));
+    }
+    if (tallies) CK(cudaMemcpyAsync(tallies, H.tallies, (size_t)H.q * 5 * 8, cudaMemcpyDefault, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  if (n_out) *n_out = n;
+  return 0;
+}
+
+int tv_hist_merge(tv_hist *h, int64_t n, const uint32_t *keys, const uint64_t *det, const uint64_t *steric,
+                  const uint64_t *rep_det, const uint64_t *rep_any, const uint8_t *w, const uint8_t *hh,
+                  const uint16_t *cells, const uint64_t *shape, const int64_t *tallies, void *stream) {
+  if (!h) return fail(TV_ERR_ARG, "null histogram");
+  if (n < 0) return fail(TV_ERR_ARG, "negative n");
+  cudaStream_t st = (cudaStream_t)stream;
+  const HistDev &H = h->H;
+  bool any_host = false;
+  {
+    Scratch S(st);
+    HistRecords R;
+    bool b[9];
+    uint64_t *d0, *d1, *d2, *d3, *d8;
+    if (int rc = stage_in(keys, n, true, S, &R.keys, b[0])) return rc;
+    if (int rc = stage_in(det, n, true, S, &d0, b[1])) return rc;
+    if (int rc = stage_in(steric, n, true, S, &d1, b[2])) return rc;
+    if (int rc = stage_in(rep_det, n, true, S, &d2, b[3])) return rc;
+    if (int rc = stage_in(rep_any, n, true, S, &d3, b[4])) return rc;
+    if (int rc = stage_in(w, n, true, S, &R.w, b[5])) return rc;
+    if (int rc = stage_in(hh, n, true, S, &R.h, b[6])) return rc;
+    if (int rc = stage_in(cells, n, true, S, &R.cells, b[7])) return rc;
+    if (int rc = stage_in(shape, (size_t)n * H.W, true, S, &d8, b[8])) return rc;
+    R.det = reinterpret_cast<unsigned long long *>(d0);
+    R.steric = reinterpret_cast<unsigned long long *>(d1);
+    R.rep_det = reinterpret_cast<unsigned long long *>(d2);
+    R.rep_any = reinterpret_cast<unsigned long long *>(d3);
+    R.shape = reinterpret_cast<unsigned long long *>(d8);
+    for (bool x : b) any_host = any_host || x;
+    long long *dt = nullptr;
+    if (tallies) {
+      CK(S.get(&dt, (size_t)H.q * 5));
+      CK(cudaMemcpyAsync(dt, tallies, (size_t)H.q * 5 * 8, cudaMemcpyDefault, st));
+      any_host = true;
+    }
+    const int blocks = (int)std::min<int64_t>(256, std::max<int64_t>(1, (n + 255) / 256));
+    k_hist_merge<<<blocks, 256, 0, st>>>(H, n, R, dt);
+    CK(cudaGetLastError());
+  }
+  if (any_host) CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+static int enumerate_common(const uint64_t *indices, uint64_t start, uint64_t chunk, uint64_t stride,
+                            int64_t count, int32_t a, int32_t bpl,
+                            const int64_t *mask_pos, const uint8_t *mask_val, int64_t m, const int64_t *free_pos,
+                            int64_t nfree, int32_t d, const int64_t *ks, int64_t q, int32_t hist_k, uint64_t seed,
+                            int32_t strict, tv_hist *h, void *stream) {
+  if (!h) return fail(TV_ERR_ARG, "null histogram");
+  if (count < 0) return fail(TV_ERR_ARG, "negative count");
+  Common C;
+  if (int rc = fill_common(a, bpl, mask_pos, mask_val, m, free_pos, nfree, d, ks, q, hist_k, seed, strict, C)) return rc;
+  if (q != h->H.q) return fail(TV_ERR_ARG, "histogram was created for q=%d, got %lld", h->H.q, (long long)q);
+  if ((int64_t)h->H.W * 64 < (int64_t)(d - 2) * (d - 2)) return fail(TV_ERR_ARG, "histogram W too small for d=%d", d);
+  cudaStream_t st = (cudaStream_t)stream;
+  bool host = false;
+  {
+    Scratch S(st);
+    uint64_t *d_idx = nullptr;
+    if (indices) {
+      if (int rc = stage_in(indices, (size_t)count, true, S, &d_idx, host)) return rc;
+    }
+    C.P.indices = d_idx;
+    C.P.start = start;
+    C.P.chunk = chunk;
+    C.P.stride = stride;
+    C.P.n = count;
+    C.P.hist_mode = 1;
+    C.P.hist = h->H;
+    if (int rc = launch_classify(C, S, st)) return rc;
+  }
+  if (host) CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int tv_enumerate_range(uint64_t start, uint64_t count, int32_t a, int32_t bpl, const int64_t *mask_pos,
+                       const uint8_t *mask_val, int64_t m, const int64_t *free_pos, int64_t nfree, int32_t d,
+                       const int64_t *ks, int64_t q, int32_t hist_k, uint64_t seed, int32_t strict, tv_hist *h,
+                       void *stream) {
+  if (count > ((uint64_t)1 << 62)) return fail(TV_ERR_ARG, "count too large for one call");
+  return enumerate_common(nullptr, start, 0, 0, (int64_t)count, a, bpl, mask_pos, mask_val, m, free_pos, nfree, d, ks, q,
+                          hist_k, seed, strict, h, stream);
+}
+
+int tv_enumerate_chunks(uint64_t start, uint64_t count, uint64_t chunk, uint64_t stride, int32_t a, int32_t bpl,
+                        const int64_t *mask_pos, const uint8_t *mask_val, int64_t m, const int64_t *free_pos,
+                        int64_t nfree, int32_t d, const int64_t *ks, int64_t q, int32_t hist_k, uint64_t seed,
+                        int32_t strict, tv_hist *h, void *stream) {
+  if (count > ((uint64_t)1 << 62)) return fail(TV_ERR_ARG, "count too large for one call");
+  if (chunk == 0 || stride < chunk) return fail(TV_ERR_ARG, "need 0 < chunk <= stride");
+  return enumerate_common(nullptr, start, chunk, stride, (int64_t)count, a, bpl, mask_pos, mask_val, m, free_pos,
+                          nfree, d, ks, q, hist_k, seed, strict, h, stream);
+}
+
+int tv_enumerate_indices(const uint64_t *indices, int64_t n, int32_t a, int32_t bpl, const int64_t *mask_pos,
+                         const uint8_t *mask_val, int64_t m, const int64_t *free_pos, int64_t nfree, int32_t d,
+                         const int64_t *ks, int64_t q, int32_t hist_k, uint64_t seed, int32_t strict, tv_hist *h,
+                         void *stream) {
+  if (!indices && n > 0) return fail(TV_ERR_ARG, "null indices");
+  return enumerate_common(indices, 0, 0, 0, n, a, bpl, mask_pos, mask_val, m, free_pos, nfree, d, ks, q, hist_k, seed,
+                          strict, h, stream);
+}
+
+int tv_int_peak_launch(int64_t iters, int32_t blocks, int32_t threads, void *stream, double *ops) {
+  int dev;
+  if (int rc = current_device(&dev)) return rc;
+  static uint32_t *sink = nullptr;
+  if (!sink) CK(cudaMalloc(&sink, 4));
+  k_int_peak<<<blocks, threads, 0, (cudaStream_t)stream>>>(iters, 12345u, sink);
+  CK(cudaGetLastError());
+  if (ops) *ops = (double)blocks * threads * (double)iters * 16.0;
+  return 0;
+}
+
+int tv_sm_count(int32_t *n) {
+  int dev;
+  if (int rc = current_device(&dev)) return rc;
+  CK(cudaDeviceGetAttribute(n, cudaDevAttrMultiProcessorCount, dev));
+  return 0;
+}
+
+}  // extern "C"

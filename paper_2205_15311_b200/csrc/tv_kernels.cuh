@@ -1,0 +1,167 @@
+// tv_kernels.cuh -- generic / single-genome / histogram maintenance kernels.
+#pragma once
+#include "tv_generic.cuh"
+
+namespace tvb {
+
+// Thread-per-genome classify over global scratch (general spaces).
+__global__ void __launch_bounds__(128) k_classify_generic(const __grid_constant__ ClassifyParams P) {
+  const int64_t T = P.g_threads;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  GView V{P.g_grid, P.g_mark, P.g_stack, P.g_placed, T, t};
+  uint32_t *rh = P.run_hash + t;  // run r at rh[r*T]
+  uint8_t edges[16 * 16];
+  for (int64_t item = t; item < P.n; item += T) {
+    const uint64_t idx = item_index(P.indices, P.start, P.chunk, P.stride, item);
+    g_decode(P.dec, P.a, idx, edges);
+    GFold F = g_classify(edges, P.a, P.d, P.kmax, P.hist_k, P.seed, idx, P.strict, V, rh, T, nullptr, 0);
+    if (F.status != 0) {
+      if (!P.hist_mode) {
+        for (int k = 0; k < P.q; k++) P.out_class[item * P.q + k] = (uint8_t)CLS_ERROR;
+      } else {
+        for (int k = 0; k < P.q; k++) atomicAdd(&P.hist.tallies[k * 5 + 4], 1ULL);
+      }
+      continue;
+    }
+    for (int k = 0; k < P.q; k++) {
+      const int c = class_at(P.ks[k], F.trivial_at, F.first_unbound, F.first_mismatch);
+      if (!P.hist_mode) P.out_class[item * P.q + k] = (uint8_t)c;
+      else atomicAdd(&P.hist.tallies[k * 5 + c], 1ULL);
+    }
+    const int hc = class_at(P.hist_k, F.trivial_at, F.first_unbound, F.first_mismatch);
+    if (hc != CLS_DET && hc != CLS_STERIC) {
+      if (!P.hist_mode) { P.out_hash[item] = 0; P.out_w[item] = 0; P.out_h[item] = 0; P.out_cells[item] = 0; }
+      continue;
+    }
+    unsigned long long *dst = nullptr;
+    int64_t W = 0, g = -1;
+    if (!P.hist_mode) {
+      dst = P.out_shape + item * P.W;
+      W = P.W;
+    } else {
+      bool gnew = false;
+      g = hist_claim(P.hist, F.hash, gnew);
+      if (g < 0) continue;
+      const bool det = hc == CLS_DET;
+      atomicAdd(det ? &P.hist.det[g] : &P.hist.steric[g], 1ULL);
+      if (det) hist_min(&P.hist.rep_det[g], idx);
+      hist_min(&P.hist.rep_any[g], idx);
+      if (!gnew) continue;
+      dst = P.hist.shape + g * P.hist.W;
+      W = P.hist.W;
+    }
+    // replay the attributed run (identical substream) to emit its bitmap
+    GRun R = g_assemble(edges, P.a, P.d, P.strict, P.seed, idx, F.attr_run, V);
+    int w, h, nc;
+    g_hash_region(V, P.d, R, w, h, nc, dst, W);
+    g_cleanup(V, R);
+    if (!P.hist_mode) {
+      P.out_hash[item] = F.hash;
+      P.out_w[item] = (uint8_t)w; P.out_h[item] = (uint8_t)h; P.out_cells[item] = (uint16_t)nc;
+    } else {
+      P.hist.whc[g] = (uint32_t)w | ((uint32_t)h << 8) | ((uint32_t)nc << 16);
+    }
+  }
+}
+
+// classify_single (_k:471-484) on one device thread; out[0..5] = status, cls, hash, w, h, cells
+__global__ void k_classify_single(const uint8_t *edges_in, int a, int d, int k, uint64_t seed, uint64_t gi,
+                                  int strict, unsigned long long *shape, int64_t W, int32_t *out,
+                                  int16_t *grid, uint8_t *mark, int32_t *stack, int32_t *placed, uint32_t *rh) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  uint8_t edges[16 * 16];
+  for (int i = 0; i < a * 16; i++) edges[i] = edges_in[i];
+  GView V{grid, mark, stack, placed, 1, 0};
+  GFold F = g_classify(edges, a, d, k, k, seed, gi, strict, V, rh, 1, shape, W);
+  out[0] = F.status;
+  out[1] = class_at(k, F.trivial_at, F.first_unbound, F.first_mismatch);
+  out[2] = (int32_t)F.hash;
+  out[3] = F.w; out[4] = F.h; out[5] = F.cells;
+}
+
+// assemble_single (_k:455-468); out[0..5] = outcome, minr, minc, maxr, maxc, n_placed
+__global__ void k_assemble_single(const uint8_t *edges_in, int a, int d, uint64_t seed, uint64_t gi, int run,
+                                  int strict, int16_t *grid, uint8_t *mark, int32_t *stack, int32_t *placed,
+                                  int32_t *out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  uint8_t edges[16 * 16];
+  for (int i = 0; i < a * 16; i++) edges[i] = edges_in[i];
+  GView V{grid, mark, stack, placed, 1, 0};
+  GRun R = g_assemble(edges, a, d, strict, seed, gi, run, V);
+  out[0] = R.outcome; out[1] = R.minr; out[2] = R.minc; out[3] = R.maxr; out[4] = R.maxc; out[5] = R.n_placed;
+}
+
+__global__ void k_fill_i16(int16_t *p, int64_t n, int16_t v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+__global__ void k_oat(const uint8_t *p, int64_t n, uint32_t *out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  uint32_t h = 0;
+  for (int64_t i = 0; i < n; i++) h = oat_step(h, p[i]);
+  *out = oat_final(h);
+}
+
+// ---- histogram maintenance
+__global__ void k_hist_reset(HistDev H) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < H.cap; s += (int64_t)gridDim.x * blockDim.x) {
+    H.keys[s] = 0ULL; H.det[s] = 0ULL; H.steric[s] = 0ULL;
+    H.rep_det[s] = ~0ULL; H.rep_any[s] = ~0ULL; H.whc[s] = 0u;
+  }
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < H.q * 5; i += blockDim.x) H.tallies[i] = 0ULL;
+    if (threadIdx.x == 0) { *H.n_keys = 0u; *H.overflow = 0u; }
+  }
+}
+
+__global__ void k_hist_compact(HistDev H, uint32_t *keys_out, uint32_t *slot_out, unsigned int *cnt) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < H.cap; s += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = H.keys[s];
+    if (k) {
+      const unsigned int p = atomicAdd(cnt, 1u);
+      keys_out[p] = (uint32_t)k;
+      slot_out[p] = (uint32_t)s;
+    }
+  }
+}
+
+struct HistRecords {  // SoA record arrays (device)
+  uint32_t *keys;
+  unsigned long long *det, *steric, *rep_det, *rep_any;
+  uint8_t *w, *h;
+  uint16_t *cells;
+  unsigned long long *shape;  // n * W
+};
+
+__global__ void k_hist_gather(HistDev H, const uint32_t *slots, int64_t n, HistRecords R) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = slots[i];
+    R.det[i] = H.det[s]; R.steric[i] = H.steric[s];
+    R.rep_det[i] = H.rep_det[s]; R.rep_any[i] = H.rep_any[s];
+    const uint32_t whc = H.whc[s];
+    R.w[i] = (uint8_t)(whc & 255u); R.h[i] = (uint8_t)((whc >> 8) & 255u); R.cells[i] = (uint16_t)(whc >> 16);
+    for (int j = 0; j < H.W; j++) R.shape[i * H.W + j] = H.shape[s * H.W + j];
+  }
+}
+
+__global__ void k_hist_merge(HistDev H, int64_t n, HistRecords R, const long long *tallies) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    bool gnew = false;
+    const int64_t g = hist_claim(H, R.keys[i], gnew);
+    if (g < 0) continue;
+    if (R.det[i]) atomicAdd(&H.det[g], R.det[i]);
+    if (R.steric[i]) atomicAdd(&H.steric[g], R.steric[i]);
+    if (R.rep_det[i] != ~0ULL) hist_min(&H.rep_det[g], R.rep_det[i]);
+    if (R.rep_any[i] != ~0ULL) hist_min(&H.rep_any[g], R.rep_any[i]);
+    if (gnew) {
+      H.whc[g] = (uint32_t)R.w[i] | ((uint32_t)R.h[i] << 8) | ((uint32_t)R.cells[i] << 16);
+      for (int j = 0; j < H.W; j++) H.shape[g * H.W + j] = R.shape[i * H.W + j];
+    }
+  }
+  if (tallies && blockIdx.x == 0)
+    for (int i = threadIdx.x; i < H.q * 5; i += blockDim.x)
+      if (tallies[i]) atomicAdd(&H.tallies[i], (unsigned long long)tallies[i]);
+}
+
+}  // namespace tvb

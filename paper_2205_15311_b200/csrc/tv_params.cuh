@@ -1,0 +1,46 @@
+// tv_params.cuh -- launch parameter blocks shared by host (tv_capi.cu) and kernels.
+#pragma once
+#include <cstdint>
+#include "tv_device.cuh"
+#include "tv_hist.cuh"
+
+namespace tvb {
+
+constexpr int kMaxKs = 64;
+
+struct ClassifyParams {
+  LabelDecoder dec;
+  const uint64_t *indices;  // classify mode: enumeration indices; nullptr in range mode
+  uint64_t start;           // range mode: item i -> index start + (i / chunk) * stride + (i % chunk)
+  uint64_t chunk, stride;   // chunk == 0: plain range start + i
+  int64_t n;                // work items
+  int32_t a, d, strict, q, kmax, hist_k;
+  int32_t ks[kMaxKs];       // ascending prefix redundancies (_k:410-413)
+  uint64_t seed;
+  // classify_batch outputs (_k:404-452), all device pointers
+  uint8_t *out_class;
+  uint32_t *out_hash;
+  uint8_t *out_w, *out_h;
+  uint16_t *out_cells;
+  unsigned long long *out_shape;
+  int64_t W;
+  // histogram mode (enumerate_range): no per-genome outputs
+  int32_t hist_mode;
+  HistDev hist;
+  // scratch
+  uint32_t *run_hash;       // per lane, kmax entries
+  uint16_t *spill;          // fast kernel: per lane stack entries beyond the shared-memory part
+  int32_t S;                // fast kernel: shared-memory stack capacity (entries, multiple of 2)
+  int32_t spill_cap;        // d*d - S
+  int32_t GW;               // fast kernel: grid words per lane
+  int32_t cta_slots;        // fast kernel: per-CTA shared histogram slots (power of 2; 0 = off)
+  unsigned long long *work; // dynamic work counter
+  // generic kernel scratch (per thread, interleaved)
+  int16_t *g_grid;
+  uint8_t *g_mark;
+  int32_t *g_stack;
+  int32_t *g_placed;
+  int64_t g_threads;
+};
+
+}  // namespace tvb

@@ -1,0 +1,120 @@
+"""Multi-GPU enumeration: index-range sharding plus one histogram exchange.
+
+Enumeration shards naturally -- every genome's substream is keyed by
+(seed, enumeration index, run) (_k:45-48), so which rank processes an index
+cannot change its result.  Chunks are dealt round-robin (chunk c -> rank
+c mod R) because work varies strongly with the high index bits (the seed
+tile's labels).  The only exchange is at the end: the per-rank histograms are
+combined by ``allreduce_histogram`` -- an all-gather of the (tiny) key sets to
+build the same sorted key union on every rank, then dense all-reduces over
+that union: SUM for counts and class tallies, MIN for representatives, MAX
+for the payload (identical wherever present).  With the NCCL backend the
+tensors live in HBM and the collectives run over NVLink; the same code runs on
+gloo/CPU for the multi-process tests.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .classify import DeviceHistogram, Histogram, _space_meta, chunk_plan, shape_words_for
+
+I64_MAX = np.iinfo(np.int64).max
+I64_MIN = np.iinfo(np.int64).min
+U64_MAX = np.iinfo(np.uint64).max
+
+
+def _dev(group):
+    import torch
+    import torch.distributed as dist
+    backend = dist.get_backend(group)
+    if backend == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def allreduce_histogram(h: Histogram, group=None) -> Histogram:
+    """Combine per-rank histograms; every rank returns the identical merged result."""
+    import torch
+    import torch.distributed as dist
+
+    dev = _dev(group)
+    world = dist.get_world_size(group)
+    n = torch.tensor([len(h)], dtype=torch.int64, device=dev)
+    ns = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(ns, n, group=group)
+    nmax = max(int(x.item()) for x in ns)
+    kp = torch.full((max(nmax, 1),), -1, dtype=torch.int64, device=dev)
+    if len(h):
+        kp[: len(h)] = torch.from_numpy(h.keys.astype(np.int64)).to(dev)
+    allk = [torch.empty_like(kp) for _ in range(world)]
+    dist.all_gather(allk, kp, group=group)
+    union = torch.unique(torch.cat(allk))
+    union = union[union >= 0]
+    U = int(union.numel())
+    pos = torch.searchsorted(union, torch.from_numpy(h.keys.astype(np.int64)).to(dev))
+    q5 = h.tallies.size
+    sums = torch.zeros(2 * U + q5, dtype=torch.int64, device=dev)
+    sums[pos] = torch.from_numpy(h.det.astype(np.int64)).to(dev)
+    sums[U + pos] = torch.from_numpy(h.steric.astype(np.int64)).to(dev)
+    sums[2 * U:] = torch.from_numpy(h.tallies.reshape(-1).astype(np.int64)).to(dev)
+    mins = torch.full((2 * U,), I64_MAX, dtype=torch.int64, device=dev)
+
+    def rep(a):
+        r = a.astype(np.uint64)
+        return torch.from_numpy(np.where(r == U64_MAX, I64_MAX, r.astype(np.int64))).to(dev)
+    mins[pos] = rep(h.rep_det)
+    mins[U + pos] = rep(h.rep_any)
+    W = h.W
+    maxs = torch.full((U, 1 + W), I64_MIN, dtype=torch.int64, device=dev)
+    whc = h.w.astype(np.int64) | (h.h.astype(np.int64) << 8) | (h.cells.astype(np.int64) << 16)
+    maxs[pos, 0] = torch.from_numpy(whc).to(dev)
+    maxs[pos, 1:] = torch.from_numpy(np.ascontiguousarray(h.shape).view(np.int64)).to(dev)
+    dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
+    dist.all_reduce(mins, op=dist.ReduceOp.MIN, group=group)
+    dist.all_reduce(maxs, op=dist.ReduceOp.MAX, group=group)
+    s = sums.cpu().numpy()
+    m = mins.cpu().numpy()
+    x = maxs.cpu().numpy()
+    out = Histogram(h.ks, h.hist_k, W, meta=dict(h.meta))
+    out.keys = union.cpu().numpy().astype(np.uint32)
+    out.det = s[:U].astype(np.uint64)
+    out.steric = s[U:2 * U].astype(np.uint64)
+    out.tallies = s[2 * U:].reshape(h.tallies.shape).astype(np.int64)
+
+    def unrep(a):
+        return np.where(a == I64_MAX, U64_MAX, a.astype(np.uint64)).astype(np.uint64)
+    out.rep_det = unrep(m[:U])
+    out.rep_any = unrep(m[U:])
+    out.w = (x[:, 0] & 0xFF).astype(np.uint8)
+    out.h = ((x[:, 0] >> 8) & 0xFF).astype(np.uint8)
+    out.cells = ((x[:, 0] >> 16) & 0xFFFF).astype(np.uint16)
+    out.shape = np.ascontiguousarray(x[:, 1:]).view(np.uint64).reshape(U, W)
+    return out
+
+
+def rank_chunks(plan: list, rank: int, world: int) -> list:
+    """Round-robin assignment of enumeration chunks to ranks."""
+    return [c for i, c in enumerate(plan) if i % world == rank]
+
+
+def enumerate_space_distributed(space, d: int = 19, k: int = 8, seed: int = 0, batch_size: int = 1 << 22, *,
+                                ks=None, hist_k: int | None = None, strict: bool = True, start: int = 0,
+                                count: int | None = None, capacity: int = 1 << 20, group=None) -> Histogram:
+    """enumerate_space over all ranks of ``group`` (one GPU per rank)."""
+    import torch.distributed as dist
+    ks = tuple(sorted(int(x) for x in (ks if ks is not None else (k,))))
+    hist_k = int(hist_k if hist_k is not None else ks[-1])
+    if count is None:
+        count = space.cardinality - start
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    plan = rank_chunks(chunk_plan(start, count, batch_size), rank, world)
+    dev = DeviceHistogram(ks, hist_k, shape_words_for(d), capacity)
+    try:
+        for s, n in plan:
+            dev.enumerate_range(space, s, n, d, seed, strict)
+        local = dev.export(meta=_space_meta(space, d, seed, strict))
+    finally:
+        dev.close()
+    out = allreduce_histogram(local, group)
+    out.meta.update(start=int(start), count=int(count), world=world)
+    return out
