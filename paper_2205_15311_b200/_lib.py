@@ -77,9 +77,10 @@ def lib():
     """The loaded library; raises if it has not been built."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise TvError(f"CUDA extension missing: {LIB_PATH} (run __graft_entry__.build())")
-        L = ctypes.CDLL(LIB_PATH)
+        path = os.environ.get("TV_LIB_PATH", LIB_PATH)  # alternate build for A/B measurements
+        if not os.path.exists(path):
+            raise TvError(f"CUDA extension missing: {path} (run __graft_entry__.build())")
+        L = ctypes.CDLL(path)
         for name, (res, args) in _SIGS.items():
             f = getattr(L, name)
             f.restype = res

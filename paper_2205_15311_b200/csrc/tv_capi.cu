@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -175,7 +176,10 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
   if (C.fast) {
     const int PD = d + 2;
     P.GW = (PD * PD + 7) / 8;
-    P.S = std::min(64, (dd + 1) & ~1);
+    const char *es = getenv("TV_STACK_S");
+    P.S = std::min(es ? std::max(4, atoi(es)) & ~1 : 64, (dd + 1) & ~1);
+    const char *et = getenv("TV_SERVICE_THRESH");
+    P.service_thresh = et ? atoi(et) : 0;
     if (P.S < 4) P.S = 4;
     P.spill_cap = std::max(0, dd - P.S);
     P.cta_slots = P.hist_mode ? 512 : 0;
@@ -284,8 +288,9 @@ int tv_classify_batch(const uint64_t *indices, int64_t n, int32_t a, int32_t bpl
   Common C;
   if (n < 0) return fail(TV_ERR_ARG, "negative n");
   if (int rc = fill_common(a, bpl, mask_pos, mask_val, m, free_pos, nfree, d, ks, q, hist_k, seed, strict, C)) return rc;
-  const int64_t need_bits = (int64_t)(d - 2) * (d - 2);
-  if (W * 64 < need_bits) return fail(TV_ERR_ARG, "out_shape has %lld words; d=%d needs %lld", (long long)W, d, (long long)((need_bits + 63) / 64));
+  // The reference writes shape words unchecked (_k:283-291); shapes wider
+  // than W words are truncated here instead of overrunning the row.
+  if (W < 1) return fail(TV_ERR_ARG, "out_shape needs at least one word per row");
   int dev;
   if (int rc = current_device(&dev)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
@@ -335,7 +340,7 @@ int tv_classify_single(const uint8_t *edges, int32_t a, int32_t d, int32_t k, ui
   if (a < 1 || a > 16) return fail(TV_ERR_ARG, "tile count a=%d outside [1, 16]", a);
   if (d < 3 || d > 181) return fail(TV_ERR_ARG, "grid dimension d=%d outside [3, 181]", d);
   if (k < 1 || k > 4096) return fail(TV_ERR_ARG, "k=%d outside [1, 4096]", k);
-  if (W * 64 < (int64_t)(d - 2) * (d - 2)) return fail(TV_ERR_ARG, "shape buffer too small for d=%d", d);
+  if (W < 1) return fail(TV_ERR_ARG, "shape buffer needs at least one word");
   int dev;
   if (int rc = current_device(&dev)) return rc;
   cudaStream_t st = nullptr;

@@ -1,30 +1,33 @@
 // tv_fast.cuh -- the enumeration hot kernel: lane-per-genome movelist assembly
-// on a shared-memory nibble bitboard with SWAR candidate masks.
+// on a shared-memory nibble board with per-genome candidate tables.
 //
-// Covers a <= 3 tile types, b <= 8 labels, odd d with (d+2)^2 < 2^16.
+// Covers a <= 3 tile types, b <= 8 labels, d with (d+2)^2 < 2^16.
 // Bit-exact with the reference step order (_k:96-249).
 //
 // Layout (per warp, word-interleaved so lane L always hits bank L):
-//   grid  : GW words/lane; cell (r,c) of the (d+2)x(d+2) padded board is
+//   board : GW words/lane; cell (r,c) of the (d+2)x(d+2) padded board is
 //           nibble lin = r*(d+2)+c; 0..4a-1 = placed candidate t*4+orient,
 //           0xE = empty + on the movelist, 0xF = empty.
-//   stack : S u16 entries/lane (entry = r<<8 | c), spilled to global beyond S.
+//   stack : S u16 entries/lane (entry = lin), spilled to global beyond S.
 // Per CTA: a small open-addressed phenotype cache (histogram mode) and the
 // class tallies, flushed to the global table once at the end.
 //
 // Candidate scan (_k:166-209) as SWAR over nibble lanes, one nibble per
-// candidate c = t*4 + orient: E[dir] holds the label each candidate shows in
-// direction dir, so "bonds the neighbour's label p" is a nibble-equality with
-// partner(p) and "strict conflict" is nonzero & !bond.  The first hit is
-// ffs(cand); ambiguity is any other hit with a different in-situ 4-label
-// code (precomputed class ids, _k:199-205).
+// candidate c = t*4 + orient (scan order): E[dir] holds the label each
+// candidate shows in direction dir, so "bonds the neighbour's label p" is a
+// nibble-equality with partner(p) and "strict conflict" is nonzero & !bond.
+// The first hit is ffs(cand); ambiguity is any other hit whose in-situ 4-label
+// code differs (precomputed equivalence-class ids, _k:199-205).  (Per-genome
+// lookup tables indexed by neighbour value were measured slower: building
+// them costs ~900 instructions per genome in the divergent service pass.)
+//
+// Lane service (run end, k-run fold, histogram insert, refill) is divergent
+// and several times longer than a pop, so a lane whose run ended parks and
+// the warp services all parked lanes in one pass once enough accumulated.
 #pragma once
 #include "tv_params.cuh"
 
 namespace tvb {
-
-template <int A> struct FastMask { typedef uint32_t T; };
-template <> struct FastMask<3> { typedef uint64_t T; };
 
 template <typename M> __device__ __forceinline__ M rep_nib(uint32_t v) {
   return (M)v * (M)0x1111111111111111ULL;
@@ -40,9 +43,9 @@ __device__ __forceinline__ int ffs_m(uint32_t x) { return __ffs(x) - 1; }
 __device__ __forceinline__ int ffs_m(uint64_t x) { return __ffsll((long long)x) - 1; }
 
 struct FastLane {
-  uint32_t *gw;          // &grid word 0 of this lane (stride 32 words)
-  uint32_t *sw;          // &stack word 0 of this lane (stride 32 words, 2 entries per word)
-  uint16_t *spill;       // &spill entry 0 of this lane (stride 32)
+  uint32_t *gw;     // &board word 0 of this lane (stride 32 words)
+  uint32_t *sw;     // &stack word 0 of this lane (stride 32 words, 2 entries per word)
+  uint16_t *spill;  // &spill entry 0 of this lane (stride 32)
   int S;
   __device__ __forceinline__ uint32_t nib(int lin) const {
     return (gw[(lin >> 3) * 32] >> ((lin & 7) * 4)) & 15u;
@@ -62,13 +65,79 @@ struct FastLane {
   }
 };
 
+// ---- candidate tables -------------------------------------------------------
+template <int A> struct Cand;
+
+// SWAR over NC nibble lanes (NC = 4a; a <= 2 fits 32-bit masks, a == 3 64-bit):
+// E[dir] holds every candidate's dir-face label, "bonds p" is nibble-equality
+// with partner(p), CLS holds each candidate's equivalence-class id.
+template <typename M, int NC> struct CandSwar {
+  M E0, E1, E2, E3, N0, N1, N2, N3, CLS, SM;
+  static constexpr M VALID = (M)(0x8888888888888888ULL >> (64 - 4 * NC));
+
+  __device__ __forceinline__ void build(const uint32_t *lab, int ntiles, bool strict) {
+    E0 = E1 = E2 = E3 = 0;
+    uint32_t code[NC];
+#pragma unroll
+    for (int t = 0; t < NC / 4; t++) {
+#pragma unroll
+      for (int r = 0; r < 4; r++) {
+        const int c = t * 4 + r;
+        const uint32_t e0 = lab[t * 4 + ((0 - r) & 3)], e1 = lab[t * 4 + ((1 - r) & 3)];
+        const uint32_t e2 = lab[t * 4 + ((2 - r) & 3)], e3 = lab[t * 4 + ((3 - r) & 3)];
+        E0 |= (M)e0 << (4 * c); E1 |= (M)e1 << (4 * c);
+        E2 |= (M)e2 << (4 * c); E3 |= (M)e3 << (4 * c);
+        code[c] = t < ntiles ? (e0 | (e1 << 4) | (e2 << 8) | (e3 << 12)) : 0xFFFF0000u | (uint32_t)c;
+      }
+    }
+    CLS = 0;
+#pragma unroll
+    for (int c = 0; c < NC; c++) {
+      uint32_t id = (uint32_t)c;
+#pragma unroll
+      for (int c2 = NC - 1; c2 >= 0; c2--)
+        if (c2 < c && code[c2] == code[c]) id = (uint32_t)c2;
+      CLS |= (M)id << (4 * c);
+    }
+    N0 = nz_nib<M>(E0) & VALID; N1 = nz_nib<M>(E1) & VALID;
+    N2 = nz_nib<M>(E2) & VALID; N3 = nz_nib<M>(E3) & VALID;
+    SM = strict ? ~(M)0 : (M)0;
+  }
+
+  __device__ __forceinline__ M cand(uint32_t vN, uint32_t vE, uint32_t vS, uint32_t vW) const {
+    const uint32_t pN = vN < (uint32_t)NC ? get_nib<M>(E2, vN) : 0u;
+    const uint32_t pE = vE < (uint32_t)NC ? get_nib<M>(E3, vE) : 0u;
+    const uint32_t pS = vS < (uint32_t)NC ? get_nib<M>(E0, vS) : 0u;
+    const uint32_t pW = vW < (uint32_t)NC ? get_nib<M>(E1, vW) : 0u;
+    M bond = 0, conf = 0;
+#define TV_DIR(Ed, Nd, p)                                                      \
+  {                                                                            \
+    const M on = (p) ? VALID : (M)0;                                           \
+    const M bm = ~nz_nib<M>((Ed) ^ rep_nib<M>((((p) - 1u) ^ 1u) + 1u)) & on;   \
+    bond |= bm;                                                                \
+    conf |= (Nd) & ~bm & on;                                                   \
+  }
+    TV_DIR(E0, N0, pN)
+    TV_DIR(E1, N1, pE)
+    TV_DIR(E2, N2, pS)
+    TV_DIR(E3, N3, pW)
+#undef TV_DIR
+    return bond & ~(conf & SM);
+  }
+  __device__ __forceinline__ uint32_t first(M cand) const { return (uint32_t)ffs_m(cand) >> 2; }
+  __device__ __forceinline__ bool ambiguous(M cand, uint32_t cf) const {
+    return (nz_nib<M>(CLS ^ rep_nib<M>(get_nib<M>(CLS, cf))) & cand) != 0;
+  }
+};
+template <> struct Cand<3> : CandSwar<uint64_t, 12> {};
+template <> struct Cand<2> : CandSwar<uint32_t, 8> {};
+template <> struct Cand<1> : Cand<2> {};
+
 enum { ST_NEED = 0, ST_RUN = 1, ST_DONE = 2 };
 
 template <int A>
 __global__ void __launch_bounds__(256, 2) k_classify_fast(const __grid_constant__ ClassifyParams P) {
-  typedef typename FastMask<A>::T M;
   constexpr int NC = 4 * A;
-  const M VALID = (M)(0x8888888888888888ULL >> (64 - 4 * NC));
   extern __shared__ uint32_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
@@ -102,333 +171,284 @@ __global__ void __launch_bounds__(256, 2) k_classify_fast(const __grid_constant_
 
   const int d = P.d, PD = d + 2, dd = d * d;
   const uint32_t magic = (uint32_t)(0x100000000ULL / (uint64_t)PD) + 1u;
-  const int cE = ((d >> 1) + 1) * 257;  // centre entry (r<<8|c), padded coords
-  const M strict_mask = P.strict ? ~(M)0 : (M)0;
+  const int cr = (d >> 1) + 1, centre = cr * PD + cr;
+  const int thresh = P.service_thresh > 0 ? P.service_thresh : 12;
 
-  int st = ST_NEED;
+  int st = ST_NEED, pend = -1;
   int64_t item = 0;
   uint64_t idx = 0, rs = 0;
   int run = 0, replay = 0, sp = 0;
   int minr = 0, maxr = 0, minc = 0, maxc = 0;
   int trivial_at = -1, first_unbound = -1, first_mismatch = -1;
   uint32_t hash0 = 0, best = 0;
-  int64_t pslot = -1;  // histogram slot owning the payload being replayed
-  M E0 = 0, E1 = 0, E2 = 0, E3 = 0, N0 = 0, N1 = 0, N2 = 0, N3 = 0, CLS = 0;
-
-  auto start_run = [&]() {
-    rs = stream_state(P.seed, idx, (uint64_t)run);
-    const int cr = cE >> 8, cl = cr * PD + (cE & 255);
-    Ln.set_nib(cl, 0u);                                  // seed tile, orientation 0 (_k:115)
-    minr = maxr = minc = maxc = cr;
-    uint32_t nbp = 0x03020100u;                          // N,E,S,W then shuffle (_k:122-131)
-#pragma unroll
-    for (int j = 3; j > 0; j--) {
-      const uint32_t q = rng_below(rs, (uint32_t)(j + 1));
-      const uint32_t x = ((nbp >> (8 * j)) ^ (nbp >> (8 * q))) & 0xFFu;
-      nbp ^= (x << (8 * j)) | (x << (8 * q));
-    }
-#pragma unroll
-    for (int j = 0; j < 4; j++) {                        // push (_k:133-136)
-      const uint32_t dir = (nbp >> (8 * j)) & 3u;
-      const int de = dir == 0 ? -256 : dir == 1 ? 1 : dir == 2 ? 256 : -1;
-      const int dl = dir == 0 ? -PD : dir == 1 ? 1 : dir == 2 ? PD : -1;
-      Ln.st_write(j, (uint32_t)(cE + de));
-      Ln.set_nib(cl + dl, 0xEu);
-    }
-    sp = 4;
-  };
-
-  auto cleanup = [&]() {  // all marks and tiles lie inside bbox +- 1 (Appendix A.8/9)
-    const int lo = ((minr - 1) * PD + (minc - 1)) >> 3;
-    const int hi = ((maxr + 1) * PD + (maxc + 1)) >> 3;
-    for (int w = lo; w <= hi; w++) Ln.gw[w * 32] = 0xFFFFFFFFu;
-  };
-
-  // OAT over w, h, (x, y)... of the cropped shape (_k:260-277); optional pack (_k:280-292)
-  auto scan = [&](int &w, int &h, int &n, unsigned long long *out, int64_t W) -> uint32_t {
-    w = maxc - minc + 1;
-    h = maxr - minr + 1;
-    n = 0;
-    uint32_t hs = oat_step(oat_step(0u, (uint32_t)w), (uint32_t)h);
-    const int lo = (minr * PD + minc) >> 3, hi = (maxr * PD + maxc) >> 3;
-    int64_t cw = 0;
-    unsigned long long acc = 0;
-    for (int wi = lo; wi <= hi; wi++) {
-      uint32_t occ = nz_nib<uint32_t>(~Ln.gw[wi * 32]);
-      while (occ) {
-        const int b = __ffs(occ) - 1;
-        occ &= occ - 1;
-        const uint32_t L = (uint32_t)(wi * 8 + (b >> 2));
-        const uint32_t R = __umulhi(L, magic);
-        const int y = (int)R - minr, x = (int)(L - R * PD) - minc;
-        hs = oat_step(oat_step(hs, (uint32_t)x), (uint32_t)y);
-        n++;
-        if (out) {
-          const int bit = y * w + x;
-          const int64_t wj = bit >> 6;
-          while (cw < wj) { out[cw++] = acc; acc = 0; }
-          acc |= 1ULL << (bit & 63);
-        }
-      }
-    }
-    if (out) { while (cw < W) { out[cw++] = acc; acc = 0; } }
-    return oat_final(hs);
-  };
+  int64_t pslot = -1;  // histogram slot whose payload the replay writes
+  Cand<A> K;
 
   for (;;) {
-    // ---- refill lanes that need a genome (warp-aggregated work counter)
-    const unsigned need = __ballot_sync(0xFFFFFFFFu, st == ST_NEED);
-    if (need) {
-      const int leader = __ffs(need) - 1;
-      unsigned long long base = 0;
-      if (lane == leader) base = atomicAdd(P.work, (unsigned long long)__popc(need));
-      base = __shfl_sync(0xFFFFFFFFu, base, leader);
-      if (st == ST_NEED) {
-        item = (int64_t)base + __popc(need & ((1u << lane) - 1u));
-        if (item >= P.n) {
-          st = ST_DONE;
-        } else {
-          idx = item_index(P.indices, P.start, P.chunk, P.stride, item);
-          // decode labels, in-situ edge planes and equivalence ids (_k:384-401, _k:199)
-          uint32_t lab[NC];
-#pragma unroll
-          for (int te = 0; te < NC; te++) lab[te] = decode_label(P.dec, te, idx);
-          E0 = E1 = E2 = E3 = 0;
-          uint32_t code[NC];
-#pragma unroll
-          for (int t = 0; t < A; t++) {
-#pragma unroll
-            for (int r = 0; r < 4; r++) {
-              const int c = t * 4 + r;
-              const uint32_t e0 = lab[t * 4 + ((0 - r) & 3)], e1 = lab[t * 4 + ((1 - r) & 3)];
-              const uint32_t e2 = lab[t * 4 + ((2 - r) & 3)], e3 = lab[t * 4 + ((3 - r) & 3)];
-              E0 |= (M)e0 << (4 * c); E1 |= (M)e1 << (4 * c);
-              E2 |= (M)e2 << (4 * c); E3 |= (M)e3 << (4 * c);
-              code[c] = e0 | (e1 << 4) | (e2 << 8) | (e3 << 12);
+    const unsigned live = __ballot_sync(0xFFFFFFFFu, st != ST_DONE);
+    if (live == 0) break;
+    const unsigned parked = __ballot_sync(0xFFFFFFFFu, st == ST_NEED || pend >= 0);
+    const int nlive = __popc(live), npark = __popc(parked);
+    if (npark > 0 && (npark >= min(thresh, (nlive + 1) >> 1) || npark == nlive)) {
+      // =================== service pass over parked lanes ===================
+      bool start = false;
+      if (pend >= 0) {
+        const int ended = pend;
+        pend = -1;
+        // hash (+ pack on replay) the bounded shape before clearing (_k:260-292)
+        uint32_t hs = 0;
+        int w = 0, h = 0, n = 0;
+        if (ended == RUN_BOUNDED) {
+          unsigned long long *out = nullptr;
+          int64_t W = 0;
+          if (replay) {
+            out = P.hist_mode ? P.hist.shape + pslot * P.hist.W : P.out_shape + item * P.W;
+            W = P.hist_mode ? P.hist.W : P.W;
+          }
+          w = maxc - minc + 1;
+          h = maxr - minr + 1;
+          hs = oat_step(oat_step(0u, (uint32_t)w), (uint32_t)h);
+          const int lo = (minr * PD + minc) >> 3, hi = (maxr * PD + maxc) >> 3;
+          int64_t cw = 0;
+          unsigned long long acc = 0;
+          for (int wi = lo; wi <= hi; wi++) {
+            uint32_t occ = nz_nib<uint32_t>(~Ln.gw[wi * 32]);
+            while (occ) {
+              const int b = __ffs(occ) - 1;
+              occ &= occ - 1;
+              const uint32_t L = (uint32_t)(wi * 8 + (b >> 2));
+              const uint32_t R = __umulhi(L, magic);
+              const int y = (int)R - minr, x = (int)(L - R * PD) - minc;
+              hs = oat_step(oat_step(hs, (uint32_t)x), (uint32_t)y);
+              n++;
+              if (out) {
+                const int bit = y * w + x;
+                const int64_t wj = bit >> 6;
+                if (wj < W) {  // bits past the caller's W words are dropped
+                  while (cw < wj) { out[cw++] = acc; acc = 0; }
+                  acc |= 1ULL << (bit & 63);
+                }
+              }
             }
           }
-          CLS = 0;
-#pragma unroll
-          for (int c = 0; c < NC; c++) {
-            uint32_t id = (uint32_t)c;
-#pragma unroll
-            for (int c2 = NC - 1; c2 >= 0; c2--)
-              if (c2 < c && code[c2] == code[c]) id = (uint32_t)c2;
-            CLS |= (M)id << (4 * c);
+          if (out) { while (cw < W) { out[cw++] = acc; acc = 0; } }
+          hs = oat_final(hs);
+        }
+        {  // clear: every tile and movelist mark lies inside bbox +- 1
+          const int lo = ((minr - 1) * PD + (minc - 1)) >> 3;
+          const int hi = ((maxr + 1) * PD + (maxc + 1)) >> 3;
+          for (int wi = lo; wi <= hi; wi++) Ln.gw[wi * 32] = 0xFFFFFFFFu;
+        }
+        if (replay) {
+          if (!P.hist_mode) {
+            P.out_hash[item] = best;
+            P.out_w[item] = (uint8_t)w; P.out_h[item] = (uint8_t)h; P.out_cells[item] = (uint16_t)n;
+          } else {
+            P.hist.whc[pslot] = (uint32_t)w | ((uint32_t)h << 8) | ((uint32_t)n << 16);
           }
-          N0 = nz_nib<M>(E0) & VALID; N1 = nz_nib<M>(E1) & VALID;
-          N2 = nz_nib<M>(E2) & VALID; N3 = nz_nib<M>(E3) & VALID;
-          trivial_at = first_unbound = first_mismatch = -1;
-          run = 0;
-          replay = 0;
-          start_run();
-          st = ST_RUN;
+          st = ST_NEED;
+        } else {
+          // ---- fold one run (_k:323-349)
+          bool done = false;
+          if (ended == RUN_BOUNDED) {
+            rh[run * 32] = hs;
+            if (run == 0) hash0 = hs;
+            else if (first_mismatch < 0 && first_unbound != 0 && hs != hash0) first_mismatch = run;
+          } else if (ended == RUN_UNBOUND) {
+            if (first_unbound < 0) first_unbound = run;
+            rh[run * 32] = 0u;
+          } else {
+            done = true;
+            if (ended == RUN_TRIVIAL) trivial_at = run;
+          }
+          run++;
+          if (!done && run < P.kmax) {
+            start = true;
+          } else if (ended == RUN_OVERFLOW) {  // _k:434-437
+            if (!P.hist_mode) {
+              for (int k = 0; k < P.q; k++) P.out_class[item * P.q + k] = (uint8_t)CLS_ERROR;
+            } else {
+              for (int k = 0; k < P.q; k++) atomicAdd(&c_tal[k * 5 + 4], 1u);
+            }
+            st = ST_NEED;
+          } else {
+            // ---- genome fold (_k:351-381, _k:438-452)
+            if (!P.hist_mode) {
+              for (int k = 0; k < P.q; k++)
+                P.out_class[item * P.q + k] = (uint8_t)class_at(P.ks[k], trivial_at, first_unbound, first_mismatch);
+            } else {
+              for (int k = 0; k < P.q; k++)
+                atomicAdd(&c_tal[k * 5 + class_at(P.ks[k], trivial_at, first_unbound, first_mismatch)], 1u);
+            }
+            const int hc = class_at(P.hist_k, trivial_at, first_unbound, first_mismatch);
+            st = ST_NEED;
+            if (hc == CLS_DET || hc == CLS_STERIC) {
+              int attr = 0;
+              best = hash0;
+              if (hc == CLS_STERIC) {  // majority hash over the first hist_k runs, ties -> smaller
+                int best_n = 0;
+                best = 0u;
+                for (int j = 0; j < P.hist_k; j++) {
+                  const uint32_t hj = rh[j * 32];
+                  int cnt = 0;
+                  for (int l = 0; l < P.hist_k; l++) cnt += rh[l * 32] == hj;
+                  if (cnt > best_n || (cnt == best_n && hj < best)) { best_n = cnt; best = hj; }
+                }
+                if (best != hash0)
+                  for (int j = 1; j < P.hist_k; j++)
+                    if (rh[j * 32] == best) { attr = j; break; }
+              }
+              bool need_payload = true;
+              if (P.hist_mode) {
+                const bool det = hc == CLS_DET;
+                bool gnew = false, cached = false;
+                int64_t g = -1;
+                if (HS > 0) {
+                  const unsigned long long key = (1ULL << 32) | best;
+                  uint32_t s = (uint32_t)hist_home(best, HS);
+                  for (int p = 0; p < 16; p++) {
+                    unsigned long long k = *((volatile unsigned long long *)&c_key[s]);
+                    if (k == 0ULL) {
+                      k = atomicCAS(&c_key[s], 0ULL, key);
+                      if (k == 0ULL) {
+                        g = hist_claim(P.hist, best, gnew);
+                        *((volatile int32_t *)&c_gs[s]) = (int32_t)g;
+                        k = key;
+                      }
+                    }
+                    if (k == key) {
+                      atomicAdd(det ? &c_det[s] : &c_ste[s], 1u);
+                      if (det && c_rdet[s] > idx) atomicMin(&c_rdet[s], (unsigned long long)idx);
+                      if (c_rany[s] > idx) atomicMin(&c_rany[s], (unsigned long long)idx);
+                      cached = true;
+                      break;
+                    }
+                    s = (s + 1) & (uint32_t)(HS - 1);
+                  }
+                }
+                if (!cached) {
+                  g = hist_claim(P.hist, best, gnew);
+                  if (g >= 0) {
+                    atomicAdd(det ? &P.hist.det[g] : &P.hist.steric[g], 1ULL);
+                    if (det) hist_min(&P.hist.rep_det[g], idx);
+                    hist_min(&P.hist.rep_any[g], idx);
+                  }
+                }
+                need_payload = gnew;
+                pslot = g;
+              }
+              if (need_payload) {  // replay the attributed run to emit its bitmap
+                replay = 1;
+                run = attr;
+                start = true;
+                st = ST_RUN;
+              }
+            } else if (!P.hist_mode) {
+              P.out_hash[item] = 0u; P.out_w[item] = 0; P.out_h[item] = 0; P.out_cells[item] = 0;
+            }
+          }
         }
       }
+      // ---- refill lanes that need a genome (warp-aggregated work counter)
+      const unsigned need = __ballot_sync(0xFFFFFFFFu, st == ST_NEED);
+      if (need) {
+        const int leader = __ffs(need) - 1;
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(P.work, (unsigned long long)__popc(need));
+        base = __shfl_sync(0xFFFFFFFFu, base, leader);
+        if (st == ST_NEED) {
+          item = (int64_t)base + __popc(need & ((1u << lane) - 1u));
+          if (item >= P.n) {
+            st = ST_DONE;
+          } else {
+            idx = item_index(P.indices, P.start, P.chunk, P.stride, item);
+            uint32_t lab[12];  // decode labels (_k:384-401)
+#pragma unroll
+            for (int te = 0; te < 12; te++) lab[te] = te < NC ? decode_label(P.dec, te, idx) : 0u;
+            K.build(lab, A, P.strict != 0);
+            trivial_at = first_unbound = first_mismatch = -1;
+            run = 0;
+            replay = 0;
+            start = true;
+            st = ST_RUN;
+          }
+        }
+      }
+      if (start) {  // ---- run start: seed + shuffled centre neighbours (_k:110-136)
+        rs = stream_state(P.seed, idx, (uint64_t)run);
+        Ln.set_nib(centre, 0u);
+        minr = maxr = minc = maxc = cr;
+        uint32_t nbp = 0x03020100u;
+#pragma unroll
+        for (int j = 3; j > 0; j--) {
+          const uint32_t q = rng_below(rs, (uint32_t)(j + 1));
+          const uint32_t x = ((nbp >> (8 * j)) ^ (nbp >> (8 * q))) & 0xFFu;
+          nbp ^= (x << (8 * j)) | (x << (8 * q));
+        }
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          const uint32_t dir = (nbp >> (8 * j)) & 3u;
+          const int dl = (dir & 1u) ? 1 : PD;
+          const int nl = ((dir + 1u) & 2u) ? centre + dl : centre - dl;
+          Ln.st_write(j, (uint32_t)nl);
+          Ln.set_nib(nl, 0xEu);
+        }
+        sp = 4;
+      }
     }
-    if (!__any_sync(0xFFFFFFFFu, st == ST_RUN)) break;
-    if (st != ST_RUN) continue;
+    if (st != ST_RUN || pend >= 0) continue;
 
-    // ---- one movelist pop (_k:138-248)
-    int ended = -1;
+    // =================== one movelist pop (_k:138-248) ===================
     if (sp == 0) {
-      ended = RUN_BOUNDED;
-    } else {
-      const uint32_t e = Ln.st_read(--sp);
-      const int r = (int)(e >> 8), c = (int)(e & 255u);
-      const int lin = r * PD + c;
-      const uint32_t vN = Ln.nib(lin - PD), vE = Ln.nib(lin + 1);
-      const uint32_t vS = Ln.nib(lin + PD), vW = Ln.nib(lin - 1);
-      M bond = 0, conf = 0;
-      {
-        // label each occupied neighbour shows toward this cell (_k:145-164); absent == inert
-        const uint32_t pN = vN < (uint32_t)NC ? get_nib<M>(E2, vN) : 0u;
-        const uint32_t pE = vE < (uint32_t)NC ? get_nib<M>(E3, vE) : 0u;
-        const uint32_t pS = vS < (uint32_t)NC ? get_nib<M>(E0, vS) : 0u;
-        const uint32_t pW = vW < (uint32_t)NC ? get_nib<M>(E1, vW) : 0u;
-#define TV_DIR(Ed, Nd, p)                                                        \
-  {                                                                              \
-    const M on = (p) ? VALID : (M)0;                                             \
-    const M bm = ~nz_nib<M>((Ed) ^ rep_nib<M>((((p) - 1u) ^ 1u) + 1u)) & on;     \
-    bond |= bm;                                                                  \
-    conf |= (Nd) & ~bm & on;                                                     \
-  }
-        TV_DIR(E0, N0, pN)
-        TV_DIR(E1, N1, pE)
-        TV_DIR(E2, N2, pS)
-        TV_DIR(E3, N3, pW)
-#undef TV_DIR
-      }
-      const M cand = bond & ~(conf & strict_mask);
-      if (cand == 0) {
-        Ln.set_nib(lin, 0xFu);                           // dropped, re-pushable (_k:210-211)
-      } else {
-        const uint32_t cf = (uint32_t)ffs_m(cand) >> 2;  // first hit in t-major, orient-minor order
-        const M amb = nz_nib<M>(CLS ^ rep_nib<M>(get_nib<M>(CLS, cf))) & cand;
-        if (amb) {
-          ended = RUN_TRIVIAL;                           // _k:208-209
-        } else if (r == 1 || c == 1 || r == d || c == d) {
-          ended = RUN_UNBOUND;                           // _k:212-213
-        } else {
-          Ln.set_nib(lin, cf);                           // place (_k:214-224)
-          minr = min(minr, r); maxr = max(maxr, r);
-          minc = min(minc, c); maxc = max(maxc, c);
-          uint32_t nbp = 0;
-          int m = 0;                                     // new frontier N,E,S,W (_k:225-237)
-          if (vN == 0xFu) { nbp |= 0u << (8 * m); m++; }
-          if (vE == 0xFu) { nbp |= 1u << (8 * m); m++; }
-          if (vS == 0xFu) { nbp |= 2u << (8 * m); m++; }
-          if (vW == 0xFu) { nbp |= 3u << (8 * m); m++; }
-          if (m == 3) {                                  // Fisher-Yates n=m..2 (_k:238-242)
-            const uint32_t q = rng_below(rs, 3u);
-            const uint32_t x = ((nbp >> 16) ^ (nbp >> (8 * q))) & 0xFFu;
-            nbp ^= (x << 16) | (x << (8 * q));
-          }
-          if (m >= 2) {
-            const uint32_t q = rng_below(rs, 2u);
-            const uint32_t x = ((nbp >> 8) ^ (nbp >> (8 * q))) & 0xFFu;
-            nbp ^= (x << 8) | (x << (8 * q));
-          }
-          for (int j = 0; j < m; j++) {                  // push (_k:243-248)
-            if (sp >= dd) { ended = RUN_OVERFLOW; break; }
-            const uint32_t dir = (nbp >> (8 * j)) & 3u;
-            const int de = dir == 0 ? -256 : dir == 1 ? 1 : dir == 2 ? 256 : -1;
-            const int dl = dir == 0 ? -PD : dir == 1 ? 1 : dir == 2 ? PD : -1;
-            Ln.st_write(sp++, e + de);
-            Ln.set_nib(lin + dl, 0xEu);
-          }
-        }
-      }
-    }
-    if (ended < 0) continue;
-
-    // ---- run end
-    if (replay) {
-      // replay of the attributed run: emit hash/w/h/cells + packed bitmap
-      int w, h, n;
-      if (!P.hist_mode) {
-        unsigned long long *row = P.out_shape + item * P.W;
-        scan(w, h, n, row, P.W);
-        P.out_hash[item] = best;
-        P.out_w[item] = (uint8_t)w;
-        P.out_h[item] = (uint8_t)h;
-        P.out_cells[item] = (uint16_t)n;
-      } else {
-        scan(w, h, n, P.hist.shape + pslot * P.hist.W, P.hist.W);
-        P.hist.whc[pslot] = (uint32_t)w | ((uint32_t)h << 8) | ((uint32_t)n << 16);
-      }
-      cleanup();
-      st = ST_NEED;
+      pend = RUN_BOUNDED;
       continue;
     }
-    bool genome_done = false, overflow = false;
-    if (ended == RUN_BOUNDED) {
-      int w, h, n;
-      const uint32_t hs = scan(w, h, n, nullptr, 0);
-      rh[run * 32] = hs;
-      if (run == 0) hash0 = hs;
-      else if (first_mismatch < 0 && first_unbound != 0 && hs != hash0) first_mismatch = run;  // _k:347-348
-    } else if (ended == RUN_UNBOUND) {
-      if (first_unbound < 0) first_unbound = run;
-      rh[run * 32] = 0u;
-    } else if (ended == RUN_TRIVIAL) {
-      trivial_at = run;
-      genome_done = true;
-    } else {
-      overflow = true;
-      genome_done = true;
+    const int lin = (int)Ln.st_read(--sp);
+    const uint32_t vN = Ln.nib(lin - PD), vE = Ln.nib(lin + 1);
+    const uint32_t vS = Ln.nib(lin + PD), vW = Ln.nib(lin - 1);
+    const auto cand = K.cand(vN, vE, vS, vW);
+    const uint32_t cf = K.first(cand);
+    const int r = (int)__umulhi((uint32_t)lin, magic), c = lin - r * PD;
+    bool place = false;
+    if (cand != 0) {
+      if (K.ambiguous(cand, cf)) pend = RUN_TRIVIAL;                           // _k:208-209
+      else if (r == 1 || c == 1 || r == d || c == d) pend = RUN_UNBOUND;     // _k:212-213
+      else place = true;
     }
-    cleanup();
-    run++;
-    if (!genome_done && run < P.kmax) { start_run(); continue; }
-
-    // ---- genome fold (_k:351-381, _k:434-452)
-    if (overflow) {
-      if (!P.hist_mode) {
-        for (int k = 0; k < P.q; k++) P.out_class[item * P.q + k] = (uint8_t)CLS_ERROR;
-      } else {
-        for (int k = 0; k < P.q; k++) atomicAdd(&c_tal[k * 5 + 4], 1u);
+    Ln.set_nib(lin, place ? cf : 0xFu);  // place, or drop (re-pushable, _k:210-211)
+    if (!place) continue;
+    minr = min(minr, r); maxr = max(maxr, r);                                 // _k:217-224
+    minc = min(minc, c); maxc = max(maxc, c);
+    // new frontier N,E,S,W (_k:225-237) as 2-bit direction codes, one per byte
+    uint32_t nbp = 0;
+    int m = 0;
+    if (vN == 0xFu) { nbp |= 0u << (8 * m); m++; }
+    if (vE == 0xFu) { nbp |= 1u << (8 * m); m++; }
+    if (vS == 0xFu) { nbp |= 2u << (8 * m); m++; }
+    if (vW == 0xFu) { nbp |= 3u << (8 * m); m++; }
+    if (m == 3) {                                                              // Fisher-Yates (_k:238-242)
+      const uint32_t q = rng_below(rs, 3u);
+      const uint32_t x = ((nbp >> 16) ^ (nbp >> (8 * q))) & 0xFFu;
+      nbp ^= (x << 16) | (x << (8 * q));
+    }
+    if (m >= 2) {
+      const uint32_t q = rng_below(rs, 2u);
+      const uint32_t x = ((nbp >> 8) ^ (nbp >> (8 * q))) & 0xFFu;
+      nbp ^= (x << 8) | (x << (8 * q));
+    }
+    const int mm = min(m, dd - sp);  // capacity check before each push (_k:243-245)
+#pragma unroll
+    for (int j = 0; j < 3; j++) {
+      if (j < mm) {
+        const uint32_t dir = (nbp >> (8 * j)) & 3u;
+        const int dl = (dir & 1u) ? 1 : PD;
+        const int nl = ((dir + 1u) & 2u) ? lin + dl : lin - dl;
+        Ln.st_write(sp + j, (uint32_t)nl);
+        Ln.set_nib(nl, 0xEu);
       }
-      st = ST_NEED;
-      continue;
     }
-    if (!P.hist_mode) {
-      for (int k = 0; k < P.q; k++)
-        P.out_class[item * P.q + k] = (uint8_t)class_at(P.ks[k], trivial_at, first_unbound, first_mismatch);
-    } else {
-      for (int k = 0; k < P.q; k++)
-        atomicAdd(&c_tal[k * 5 + class_at(P.ks[k], trivial_at, first_unbound, first_mismatch)], 1u);
-    }
-    const int hc = class_at(P.hist_k, trivial_at, first_unbound, first_mismatch);
-    if (hc != CLS_DET && hc != CLS_STERIC) {
-      if (!P.hist_mode) {
-        P.out_hash[item] = 0u; P.out_w[item] = 0; P.out_h[item] = 0; P.out_cells[item] = 0;
-      }
-      st = ST_NEED;
-      continue;
-    }
-    int attr = 0;
-    best = hash0;
-    if (hc == CLS_STERIC) {  // majority hash over the first hist_k runs, ties -> smaller
-      int best_n = 0;
-      best = 0u;
-      for (int j = 0; j < P.hist_k; j++) {
-        const uint32_t hj = rh[j * 32];
-        int cnt = 0;
-        for (int l = 0; l < P.hist_k; l++) cnt += rh[l * 32] == hj;
-        if (cnt > best_n || (cnt == best_n && hj < best)) { best_n = cnt; best = hj; }
-      }
-      if (best != hash0)
-        for (int j = 1; j < P.hist_k; j++)
-          if (rh[j * 32] == best) { attr = j; break; }
-    }
-    bool need_payload = true;
-    if (P.hist_mode) {
-      const bool det = hc == CLS_DET;
-      bool gnew = false;
-      int64_t g = -1;
-      bool cached = false;
-      if (HS > 0) {
-        const unsigned long long key = (1ULL << 32) | best;
-        uint32_t s = (uint32_t)hist_home(best, HS);
-        for (int p = 0; p < 16; p++) {
-          unsigned long long k = *((volatile unsigned long long *)&c_key[s]);
-          if (k == 0ULL) {
-            k = atomicCAS(&c_key[s], 0ULL, key);
-            if (k == 0ULL) {
-              g = hist_claim(P.hist, best, gnew);
-              *((volatile int32_t *)&c_gs[s]) = (int32_t)g;
-              k = key;
-            }
-          }
-          if (k == key) {
-            atomicAdd(det ? &c_det[s] : &c_ste[s], 1u);
-            if (det) atomicMin(&c_rdet[s], (unsigned long long)idx);
-            atomicMin(&c_rany[s], (unsigned long long)idx);
-            cached = true;
-            break;
-          }
-          s = (s + 1) & (uint32_t)(HS - 1);
-        }
-      }
-      if (!cached) {
-        g = hist_claim(P.hist, best, gnew);
-        if (g >= 0) {
-          atomicAdd(det ? &P.hist.det[g] : &P.hist.steric[g], 1ULL);
-          if (det) hist_min(&P.hist.rep_det[g], idx);
-          hist_min(&P.hist.rep_any[g], idx);
-        }
-      }
-      need_payload = gnew;
-      pslot = g;
-    }
-    if (need_payload) {
-      replay = 1;
-      run = attr;
-      start_run();
-    } else {
-      st = ST_NEED;
-    }
+    sp += mm;
+    if (mm < m) pend = RUN_OVERFLOW;
   }
 
   if (P.hist_mode) {

@@ -129,7 +129,7 @@ __device__ uint32_t g_hash_region(const GView &V, int d, const GRun &R, int &w, 
       if (V.G(row + x) >= 0) {
         st = oat_step(oat_step(st, (uint32_t)x), (uint32_t)y);
         n++;
-        if (out) {
+        if (out && (bit >> 6) < W) {  // bits past the caller's W words are dropped
           const int64_t wi = bit >> 6;
           while (cw < wi) { out[cw++] = acc; acc = 0; }
           acc |= 1ULL << (bit & 63);

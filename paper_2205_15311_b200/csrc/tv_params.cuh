@@ -34,6 +34,7 @@ struct ClassifyParams {
   int32_t spill_cap;        // d*d - S
   int32_t GW;               // fast kernel: grid words per lane
   int32_t cta_slots;        // fast kernel: per-CTA shared histogram slots (power of 2; 0 = off)
+  int32_t service_thresh;   // fast kernel: parked lanes that trigger a warp service pass (0 = default)
   unsigned long long *work; // dynamic work counter
   // generic kernel scratch (per thread, interleaved)
   int16_t *g_grid;
