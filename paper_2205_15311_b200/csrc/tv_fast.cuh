@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(256, 2) k_classify_fast(const __grid_constant_
   const int d = P.d, PD = d + 2, dd = d * d;
   const uint32_t magic = (uint32_t)(0x100000000ULL / (uint64_t)PD) + 1u;
   const int cr = (d >> 1) + 1, centre = cr * PD + cr;
-  const int thresh = P.service_thresh > 0 ? P.service_thresh : 12;
+  const int thresh = P.service_thresh > 0 ? P.service_thresh : 16;
 
   int st = ST_NEED, pend = -1;
   int64_t item = 0;
