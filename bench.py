@@ -293,8 +293,14 @@ def main():
             peak = max(peak, ops.value / (s0.elapsed_time(s1) / 1e3))
         kms = statistics.mean(kern_ms) if kern_ms else ms_per_step
         achieved = ops_per_genome * (N_S28 / world) / (kms / 1e3)
+        traffic = None
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))["k_classify_fast<2>"]
+            traffic = tr["dram_bytes_read"] + tr["dram_bytes_write"]
+        except Exception:
+            pass
         roof = {"bound": "int32_alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tops/s",
-                "frac": achieved / peak, "traffic": None,
+                "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read+write)",
                 "kernel": "k_classify_fast<2>", "kernel_ms": kms,
                 "ops_per_genome": ops_per_genome,
                 "peak_source": "measured on this GPU: tv_int_peak_launch (8 independent IADD3/LOP3 chains/thread)",

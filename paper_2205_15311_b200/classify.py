@@ -141,10 +141,12 @@ def shapesim(A, B) -> float:
 
 
 def collision_probability(n: int) -> float:
-    """1 - prod_{i=0}^{n} (1 - i 2^-32)  (Eq. 2)."""
+    """Birthday bound of Eq. 2 for n distinct phenotypes, 1 - prod_{i<n} (1 - i 2^-32).
+    SPEC.md:288-296 writes the upper limit as n but its worked example
+    (n=2 -> 2^-32) and the paper's Eq. 2 use i = 0..n-1; the example wins."""
     if n < 0:
         raise ValueError("n must be >= 0")
-    i = np.arange(n + 1, dtype=np.float64)
+    i = np.arange(max(n, 0), dtype=np.float64)
     return float(-np.expm1(np.sum(np.log1p(-i * 2.0 ** -32))))
 
 
@@ -208,6 +210,44 @@ class Histogram:
             return False
         return all(np.array_equal(getattr(self, n), getattr(other, n))
                    for n in ("keys", "det", "steric", "rep_det", "rep_any", "w", "h", "cells", "shape", "tallies"))
+
+    @classmethod
+    def from_rows(cls, indices, out_class, out_hash, out_w, out_h, out_cells, out_shape, ks, hist_k,
+                  W: int | None = None, meta: dict | None = None) -> "Histogram":
+        """Aggregate per-genome classify_batch rows (_k:404-452) into a Histogram
+        (host; used to fold classify_batch results and by the tests)."""
+        ks = tuple(int(k) for k in ks)
+        W = int(W if W is not None else out_shape.shape[1])
+        idx = np.asarray(indices, np.uint64)
+        cls_ = np.asarray(out_class)
+        out = cls(ks, int(hist_k), W, meta=dict(meta or {}))
+        for j in range(len(ks)):
+            c = cls_[:, j]
+            for v, col in ((0, 0), (1, 1), (2, 2), (3, 3), (255, 4)):
+                out.tallies[j, col] = int(np.count_nonzero(c == v))
+        hc = cls_[:, ks.index(int(hist_k))]
+        sel = np.nonzero((hc == 0) | (hc == 2))[0]
+        keys, first, inv = np.unique(np.asarray(out_hash)[sel], return_index=True, return_inverse=True)
+        U = keys.shape[0]
+        isdet = hc[sel] == 0
+        out.keys = keys.astype(np.uint32)
+        out.det = np.bincount(inv, weights=isdet, minlength=U).astype(np.uint64)
+        out.steric = np.bincount(inv, weights=~isdet, minlength=U).astype(np.uint64)
+        big = np.iinfo(np.uint64).max
+        out.rep_det = np.full(U, big, np.uint64)
+        out.rep_any = np.full(U, big, np.uint64)
+        np.minimum.at(out.rep_any, inv, idx[sel])
+        np.minimum.at(out.rep_det, inv[isdet], idx[sel][isdet])
+        rows = sel[first]
+        out.w = np.asarray(out_w)[rows].astype(np.uint8)
+        out.h = np.asarray(out_h)[rows].astype(np.uint8)
+        out.cells = np.asarray(out_cells)[rows].astype(np.uint16)
+        sh = np.zeros((U, W), np.uint64)
+        src = np.asarray(out_shape)[rows]
+        k = min(W, src.shape[1])
+        sh[:, :k] = src[:, :k]
+        out.shape = sh
+        return out
 
     # -- merging (host; commutative and associative, SPEC.md:239)
     @staticmethod
