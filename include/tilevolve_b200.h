@@ -137,6 +137,32 @@ int tv_enumerate_indices(const uint64_t *indices, int64_t n, int32_t a, int32_t 
                          const int64_t *ks, int64_t q, int32_t hist_k, uint64_t seed, int32_t strict,
                          tv_hist *h, void *stream);
 
+/* ---- GA generation loop (semantics in oracle/tv_ga_oracle.c) */
+typedef struct tv_ga tv_ga;
+/* n genomes of L <= 64 bits (integer = genome.to_int()); mode 0 asexual,
+ * 1 single-point crossover, 2 uniform crossover; T[L] = Poisson(lambda) CDF
+ * thresholds x 2^63 (k flips = #{j : (draw >> 1) >= T[j]}).  Population
+ * starts all-zero. */
+int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **out);
+int tv_ga_destroy(tv_ga *h);
+int tv_ga_set_population(tv_ga *h, const uint64_t *genomes, void *stream);  /* [h|d]; NULL = zeros */
+int tv_ga_get_population(tv_ga *h, uint64_t *out, void *stream);           /* [h|d] */
+int tv_ga_population_ptr(tv_ga *h, uint64_t **dev_ptr);
+/* Run generations g0 .. g0+n_gens-1 (one cooperative launch).  Per generation:
+ * fitness (Fujiyama popcount, or f_ext [d] for exactly one generation),
+ * stats best/sum/count(f >= target) [h|d] (may be NULL), stop after recording
+ * a generation with count >= 1 (stop_when 1) or >= adapt_count (2), else
+ * reproduce.  *gens_done = generations evaluated.  Synchronises. */
+int tv_ga_run(tv_ga *h, uint64_t seed, int64_t g0, int64_t n_gens, uint32_t target, int64_t adapt_count,
+              int32_t stop_when, const uint32_t *f_ext, uint32_t *best, uint64_t *sum, uint32_t *count,
+              int64_t *gens_done, void *stream);
+/* JaTAM-shape fitness of the current population read as enumeration indices of
+ * the space: f = d^2 - shapediff(target, run-0 grid) if DET at k, else 0.
+ * target_occ u8[d*d] host (seed-centred board); f_out device u32[n]. */
+int tv_ga_fitness_jatam(tv_ga *h, int32_t a, int32_t bpl, const int64_t *mask_pos, const uint8_t *mask_val,
+                        int64_t m, const int64_t *free_pos, int64_t nfree, int32_t d, int32_t k, uint64_t seed,
+                        int32_t strict, const uint8_t *target_occ, uint32_t *f_out, void *stream);
+
 /* ---- measurement helpers (bench.py roofline) */
 /* Launch the int32 ALU peak probe (IADD3/LOP3 chains); *ops = int32 ops issued. */
 int tv_int_peak_launch(int64_t iters, int32_t blocks, int32_t threads, void *stream, double *ops);

@@ -45,6 +45,15 @@ def lib():
         L.orc_classify_single.argtypes = [_p, _i32, _i32, _i32, _u64, _u64, _i32, _p, _i64, _p]
         L.orc_assemble_single.restype = _i32
         L.orc_assemble_single.argtypes = [_p, _i32, _i32, _u64, _u64, _i32, _i32, _p, _p]
+        L.orc_ga_run.restype = _i64
+        L.orc_ga_run.argtypes = [_p, _i64, _i32, _i32, _p, _u64, _i64, _i64, ctypes.c_uint32, _i64, _i32,
+                                 _p, _p, _p, _i32]
+        L.orc_ga_child.restype = _u64
+        L.orc_ga_child.argtypes = [_u64, _i64, _i64, _p, _p, _i64, _i32, _i32, _p]
+        L.orc_ga_draws.restype = None
+        L.orc_ga_draws.argtypes = [_u64, _u64, _u64, _i64, _p]
+        L.orc_ga_flip_counts.restype = None
+        L.orc_ga_flip_counts.argtypes = [_u64, _i64, _i32, _p, _p]
         L.orc_stream_draws.restype = None
         L.orc_stream_draws.argtypes = [_u64, _u64, _u64, _i64, _p]
         _lib = L
@@ -107,3 +116,37 @@ def assemble_single(edges, a, d, seed, genome_index, run_index, strict, out_grid
     lib().orc_assemble_single(_ptr(edges), a, d, int(seed), int(genome_index), run_index, int(bool(strict)),
                               _ptr(out_grid), _ptr(out))
     return tuple(int(v) for v in out)
+
+
+# ---------------------------------------------------------------- GA restatement (tv_ga_oracle.c)
+def ga_run(pop: np.ndarray, L: int, mode: int, T: np.ndarray, seed: int, g0: int, n_gens: int, target: int,
+           adapt_count: int, stop_when: int, nthreads: int = 0):
+    """Runs in place on pop (u64); returns (gens_done, best u32, sum u64, count u32)."""
+    assert pop.dtype == np.uint64 and pop.flags.c_contiguous
+    T = np.ascontiguousarray(T, np.uint64)
+    best = np.zeros(n_gens, np.uint32)
+    sm = np.zeros(n_gens, np.uint64)
+    cnt = np.zeros(n_gens, np.uint32)
+    done = lib().orc_ga_run(_ptr(pop), pop.shape[0], L, mode, _ptr(T), int(seed), g0, n_gens, target, adapt_count,
+                            stop_when, _ptr(best), _ptr(sm), _ptr(cnt), nthreads)
+    return int(done), best[:done], sm[:done], cnt[:done]
+
+
+def ga_child(seed, g, i, pop, cdf, L, mode, T) -> int:
+    pop = np.ascontiguousarray(pop, np.uint64)
+    cdf = np.ascontiguousarray(cdf, np.uint64)
+    T = np.ascontiguousarray(T, np.uint64)
+    return int(lib().orc_ga_child(int(seed), g, i, _ptr(pop), _ptr(cdf), pop.shape[0], L, mode, _ptr(T)))
+
+
+def ga_draws(seed, g, i, n) -> np.ndarray:
+    out = np.empty(n, np.uint64)
+    lib().orc_ga_draws(int(seed), g, i, n, _ptr(out))
+    return out
+
+
+def ga_flip_counts(seed, n, L, T) -> np.ndarray:
+    out = np.empty(n, np.int32)
+    T = np.ascontiguousarray(T, np.uint64)
+    lib().orc_ga_flip_counts(int(seed), n, L, _ptr(T), _ptr(out))
+    return out

@@ -64,6 +64,13 @@ _SIGS = {
                                    _u64, _i32, _p, _p]),
     "tv_enumerate_indices": (_i32, [_p, _i64, _i32, _i32, _p, _p, _i64, _p, _i64, _i32, _p, _i64, _i32, _u64, _i32,
                                     _p, _p]),
+    "tv_ga_create": (_i32, [_i64, _i32, _i32, _p, ctypes.POINTER(_p)]),
+    "tv_ga_destroy": (_i32, [_p]),
+    "tv_ga_set_population": (_i32, [_p, _p, _p]),
+    "tv_ga_get_population": (_i32, [_p, _p, _p]),
+    "tv_ga_population_ptr": (_i32, [_p, ctypes.POINTER(_p)]),
+    "tv_ga_run": (_i32, [_p, _u64, _i64, _i64, ctypes.c_uint32, _i64, _i32, _p, _p, _p, _p, _p, _p]),
+    "tv_ga_fitness_jatam": (_i32, [_p, _i32, _i32, _p, _p, _i64, _p, _i64, _i32, _i32, _u64, _i32, _p, _p, _p]),
     "tv_int_peak_launch": (_i32, [_i64, _i32, _i32, _p, _p]),
     "tv_sm_count": (_i32, [_p]),
 }
@@ -124,5 +131,5 @@ def stream_of(*arrays):
 def launch_info() -> dict:
     info = (ctypes.c_int64 * 5)()
     lib().tv_last_launch_info(info)
-    return dict(path={1: "bitboard", 2: "generic"}.get(info[0], "none"), ctas=info[1], threads=info[2],
+    return dict(path={1: "bitboard", 2: "generic", 3: "ga"}.get(info[0], "none"), ctas=info[1], threads=info[2],
                 smem=info[3], launches=info[4])

@@ -13,6 +13,7 @@
 
 #include "../../include/tilevolve_b200.h"
 #include "tv_fast.cuh"
+#include "tv_ga.cuh"
 #include "tv_kernels.cuh"
 
 using namespace tvb;
@@ -635,6 +636,152 @@ int tv_sm_count(int32_t *n) {
   if (int rc = current_device(&dev)) return rc;
   CK(cudaDeviceGetAttribute(n, cudaDevAttrMultiProcessorCount, dev));
   return 0;
+}
+
+// ---------------------------------------------------------------- GA
+struct tv_ga {
+  GaParams P;
+  int device;
+  int cur;  // which population buffer is current
+  int nblocks;
+  size_t smem;
+};
+
+int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **out) {
+  if (n < 2 || n > ((int64_t)1 << 28)) return fail(TV_ERR_ARG, "population %lld outside [2, 2^28]", (long long)n);
+  if (L < 1 || L > 64) return fail(TV_ERR_ARG, "genome length %d outside [1, 64]", L);
+  if (mode < 0 || mode > 2) return fail(TV_ERR_ARG, "reproduction mode %d not in {0,1,2}", mode);
+  if ((uint64_t)L * (uint64_t)n >= ((uint64_t)1 << 32)) return fail(TV_ERR_ARG, "L * population must be < 2^32");
+  int dev;
+  if (int rc = current_device(&dev)) return rc;
+  int nsm = 0;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  tv_ga *h = new tv_ga();
+  memset(&h->P, 0, sizeof h->P);
+  GaParams &P = h->P;
+  P.n = n; P.L = L; P.mode = mode;
+  for (int j = 0; j < 64; j++) P.T[j] = j < L ? T[j] : ~0ULL;
+  P.seg = 32;
+  P.seg_shift = 5;
+  while (P.seg * 32768 < n) { P.seg <<= 1; P.seg_shift++; }
+  P.n_coarse = (n + P.seg - 1) / P.seg;
+  h->smem = (size_t)P.n_coarse * 4;
+  CK(cudaFuncSetAttribute((const void *)k_ga_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ga_run, 1024, h->smem));
+  if (per_sm < 1) { delete h; return fail(TV_ERR_CUDA, "GA kernel does not fit one CTA per SM"); }
+  h->nblocks = nsm;
+  P.chunk = (n + h->nblocks - 1) / h->nblocks;
+  h->device = dev;
+  h->cur = 0;
+  cudaError_t e = cudaSuccess;
+  e = e ? e : cudaMalloc(&P.pop0, n * 8);
+  e = e ? e : cudaMalloc(&P.pop1, n * 8);
+  e = e ? e : cudaMalloc(&P.cdf, n * 4);
+  e = e ? e : cudaMalloc(&P.coarse, P.n_coarse * 4);
+  e = e ? e : cudaMalloc(&P.tot, (size_t)h->nblocks * 8);
+  e = e ? e : cudaMalloc(&P.done, 8);
+  e = e ? e : cudaMalloc(&P.final_buf, 4);
+  e = e ? e : cudaMemset(P.pop0, 0, n * 8);
+  if (e != cudaSuccess) { tv_ga_destroy(h); return fail(TV_ERR_CUDA, "GA allocation: %s", cudaGetErrorString(e)); }
+  *out = h;
+  return 0;
+}
+
+int tv_ga_destroy(tv_ga *h) {
+  if (!h) return 0;
+  GaParams &P = h->P;
+  cudaFree(P.pop0); cudaFree(P.pop1); cudaFree(P.cdf); cudaFree(P.coarse); cudaFree(P.tot);
+  cudaFree(P.done); cudaFree(P.final_buf);
+  delete h;
+  return 0;
+}
+
+int tv_ga_set_population(tv_ga *h, const uint64_t *genomes, void *stream) {
+  if (!h) return fail(TV_ERR_ARG, "null GA");
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long *dst = h->cur ? h->P.pop1 : h->P.pop0;
+  if (!genomes) CK(cudaMemsetAsync(dst, 0, h->P.n * 8, st));
+  else CK(cudaMemcpyAsync(dst, genomes, h->P.n * 8, cudaMemcpyDefault, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int tv_ga_get_population(tv_ga *h, uint64_t *out, void *stream) {
+  if (!h) return fail(TV_ERR_ARG, "null GA");
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemcpyAsync(out, h->cur ? h->P.pop1 : h->P.pop0, h->P.n * 8, cudaMemcpyDefault, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int tv_ga_population_ptr(tv_ga *h, uint64_t **dev_ptr) {
+  if (!h) return fail(TV_ERR_ARG, "null GA");
+  *dev_ptr = reinterpret_cast<uint64_t *>(h->cur ? h->P.pop1 : h->P.pop0);
+  return 0;
+}
+
+int tv_ga_run(tv_ga *h, uint64_t seed, int64_t g0, int64_t n_gens, uint32_t target, int64_t adapt_count,
+              int32_t stop_when, const uint32_t *f_ext, uint32_t *best, uint64_t *sum, uint32_t *count,
+              int64_t *gens_done, void *stream) {
+  if (!h) return fail(TV_ERR_ARG, "null GA");
+  if (n_gens < 1) return fail(TV_ERR_ARG, "n_gens must be >= 1");
+  if (f_ext && n_gens != 1) return fail(TV_ERR_ARG, "an external fitness vector covers exactly one generation");
+  if (f_ext && !is_device_ptr(f_ext)) return fail(TV_ERR_ARG, "external fitness must be a device pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  GaParams P = h->P;
+  if (h->cur) std::swap(P.pop0, P.pop1);
+  P.seed = seed; P.g0 = g0; P.n_gens = n_gens; P.target = target; P.adapt_count = adapt_count;
+  P.stop_when = stop_when; P.fitness = f_ext ? 1 : 0; P.f_ext = f_ext;
+  int64_t done = 0;
+  int32_t fb = 0;
+  {
+    Scratch S(st);
+    uint32_t *d_best, *d_count; unsigned long long *d_sum;
+    CK(S.get(&d_best, n_gens)); CK(S.get(&d_count, n_gens)); CK(S.get(&d_sum, n_gens));
+    CK(cudaMemsetAsync(d_best, 0, n_gens * 4, st));
+    CK(cudaMemsetAsync(d_count, 0, n_gens * 4, st));
+    CK(cudaMemsetAsync(d_sum, 0, n_gens * 8, st));
+    P.best = d_best; P.count = d_count; P.sum = d_sum;
+    void *args[] = {&P};
+    CK(cudaLaunchCooperativeKernel((const void *)k_ga_run, dim3(h->nblocks), dim3(1024), args, h->smem, st));
+    g_launch[0] = 3; g_launch[1] = h->nblocks; g_launch[2] = 1024; g_launch[3] = (int64_t)h->smem; g_launch[4] = 1;
+    CK(cudaMemcpyAsync(&done, P.done, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&fb, P.final_buf, 4, cudaMemcpyDeviceToHost, st));
+    if (best) CK(cudaMemcpyAsync(best, d_best, n_gens * 4, cudaMemcpyDefault, st));
+    if (count) CK(cudaMemcpyAsync(count, d_count, n_gens * 4, cudaMemcpyDefault, st));
+    if (sum) CK(cudaMemcpyAsync(sum, d_sum, n_gens * 8, cudaMemcpyDefault, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  h->cur ^= fb;
+  if (gens_done) *gens_done = done;
+  return 0;
+}
+
+int tv_ga_fitness_jatam(tv_ga *h, int32_t a, int32_t bpl, const int64_t *mask_pos, const uint8_t *mask_val,
+                        int64_t m, const int64_t *free_pos, int64_t nfree, int32_t d, int32_t k, uint64_t seed,
+                        int32_t strict, const uint8_t *target_occ, uint32_t *f_out, void *stream) {
+  if (!h) return fail(TV_ERR_ARG, "null GA");
+  if (d > 29) return fail(TV_ERR_ARG, "JaTAM fitness supports d <= 29");
+  if (nfree != h->P.L) return fail(TV_ERR_ARG, "GA genome length %d != %lld free bits", h->P.L, (long long)nfree);
+  if ((uint64_t)d * d * (uint64_t)h->P.n >= ((uint64_t)1 << 32)) return fail(TV_ERR_ARG, "d^2 * population must be < 2^32");
+  if (!is_device_ptr(f_out)) return fail(TV_ERR_ARG, "fitness output must be a device pointer");
+  Common C;
+  const int64_t ks[1] = {k};
+  if (int rc = fill_common(a, bpl, mask_pos, mask_val, m, free_pos, nfree, d, ks, 1, k, seed, strict, C)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  ClassifyParams &P = C.P;
+  P.fit_mode = 1;
+  P.out_fit = f_out;
+  int tc = 0;
+  for (int r = 0; r < d; r++)
+    for (int c = 0; c < d; c++)
+      if (target_occ[r * d + c]) { P.target_rows[r + 1] |= 1u << (c + 1); tc++; }
+  P.target_cells = tc;
+  P.indices = reinterpret_cast<const uint64_t *>(h->cur ? h->P.pop1 : h->P.pop0);
+  P.n = h->P.n;
+  Scratch S(st);
+  return launch_classify(C, S, st);
 }
 
 }  // extern "C"

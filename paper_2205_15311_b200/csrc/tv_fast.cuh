@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(256, 2) k_classify_fast(const __grid_constant_
   int run = 0, replay = 0, sp = 0;
   int minr = 0, maxr = 0, minc = 0, maxc = 0;
   int trivial_at = -1, first_unbound = -1, first_mismatch = -1;
-  uint32_t hash0 = 0, best = 0;
+  uint32_t hash0 = 0, best = 0, fit0 = 0;
   int64_t pslot = -1;  // histogram slot whose payload the replay writes
   Cand<A> K;
 
@@ -197,7 +197,8 @@ __global__ void __launch_bounds__(256, 2) k_classify_fast(const __grid_constant_
         pend = -1;
         // hash (+ pack on replay) the bounded shape before clearing (_k:260-292)
         uint32_t hs = 0;
-        int w = 0, h = 0, n = 0;
+        int w = 0, h = 0, n = 0, ov = 0;
+        const bool fit_scan = P.fit_mode && !replay && run == 0;  // overlap with the GA target shape
         if (ended == RUN_BOUNDED) {
           unsigned long long *out = nullptr;
           int64_t W = 0;
@@ -218,9 +219,11 @@ __global__ void __launch_bounds__(256, 2) k_classify_fast(const __grid_constant_
               occ &= occ - 1;
               const uint32_t L = (uint32_t)(wi * 8 + (b >> 2));
               const uint32_t R = __umulhi(L, magic);
-              const int y = (int)R - minr, x = (int)(L - R * PD) - minc;
+              const int col = (int)(L - R * PD);
+              const int y = (int)R - minr, x = col - minc;
               hs = oat_step(oat_step(hs, (uint32_t)x), (uint32_t)y);
               n++;
+              if (fit_scan) ov += (P.target_rows[R] >> col) & 1u;
               if (out) {
                 const int bit = y * w + x;
                 const int64_t wj = bit >> 6;
@@ -252,7 +255,7 @@ __global__ void __launch_bounds__(256, 2) k_classify_fast(const __grid_constant_
           bool done = false;
           if (ended == RUN_BOUNDED) {
             rh[run * 32] = hs;
-            if (run == 0) hash0 = hs;
+            if (run == 0) { hash0 = hs; fit0 = (uint32_t)n | ((uint32_t)ov << 16); }
             else if (first_mismatch < 0 && first_unbound != 0 && hs != hash0) first_mismatch = run;
           } else if (ended == RUN_UNBOUND) {
             if (first_unbound < 0) first_unbound = run;
@@ -264,6 +267,11 @@ __global__ void __launch_bounds__(256, 2) k_classify_fast(const __grid_constant_
           run++;
           if (!done && run < P.kmax) {
             start = true;
+          } else if (P.fit_mode) {  // GA JaTAM-shape fitness: d^2 - shapediff for DET, else 0
+            const int hc = ended == RUN_OVERFLOW ? CLS_ERROR : class_at(P.hist_k, trivial_at, first_unbound, first_mismatch);
+            const int diff = P.target_cells + (int)(fit0 & 0xFFFFu) - 2 * (int)(fit0 >> 16);
+            P.out_fit[item] = hc == CLS_DET ? (uint32_t)(dd - diff) : 0u;
+            st = ST_NEED;
           } else if (ended == RUN_OVERFLOW) {  // _k:434-437
             if (!P.hist_mode) {
               for (int k = 0; k < P.q; k++) P.out_class[item * P.q + k] = (uint8_t)CLS_ERROR;

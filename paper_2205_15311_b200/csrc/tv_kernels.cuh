@@ -16,6 +16,20 @@ __global__ void __launch_bounds__(128) k_classify_generic(const __grid_constant_
     const uint64_t idx = item_index(P.indices, P.start, P.chunk, P.stride, item);
     g_decode(P.dec, P.a, idx, edges);
     GFold F = g_classify(edges, P.a, P.d, P.kmax, P.hist_k, P.seed, idx, P.strict, V, rh, T, nullptr, 0);
+    if (P.fit_mode) {  // GA JaTAM-shape fitness (see ClassifyParams)
+      uint32_t fit = 0;
+      if (F.status == 0 && class_at(P.hist_k, F.trivial_at, F.first_unbound, F.first_mismatch) == CLS_DET) {
+        GRun R = g_assemble(edges, P.a, P.d, P.strict, P.seed, idx, 0, V);
+        int ov = 0, nc = 0;
+        for (int r = R.minr; r <= R.maxr; r++)
+          for (int c = R.minc; c <= R.maxc; c++)
+            if (V.G(r * P.d + c) >= 0) { nc++; ov += (P.target_rows[r + 1] >> (c + 1)) & 1u; }
+        g_cleanup(V, R);
+        fit = (uint32_t)(P.d * P.d - (P.target_cells + nc - 2 * ov));
+      }
+      P.out_fit[item] = fit;
+      continue;
+    }
     if (F.status != 0) {
       if (!P.hist_mode) {
         for (int k = 0; k < P.q; k++) P.out_class[item * P.q + k] = (uint8_t)CLS_ERROR;

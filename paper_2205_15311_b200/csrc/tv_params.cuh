@@ -27,6 +27,13 @@ struct ClassifyParams {
   // histogram mode (enumerate_range): no per-genome outputs
   int32_t hist_mode;
   HistDev hist;
+  // GA fitness mode (JaTAM-shape fitness): out_fit[i] =
+  // d^2 - shapediff(target, run-0 grid) for genomes DET at hist_k, else 0.
+  // target_rows[R] bit C = target occupancy of padded cell (R, C) (d <= 29).
+  int32_t fit_mode;
+  int32_t target_cells;
+  uint32_t *out_fit;
+  uint32_t target_rows[32];
   // scratch
   uint32_t *run_hash;       // per lane, kmax entries
   uint16_t *spill;          // fast kernel: per lane stack entries beyond the shared-memory part

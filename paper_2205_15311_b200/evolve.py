@@ -1,0 +1,340 @@
+"""Bitstring genetic algorithm (SPEC.md evolve module).
+
+The reference ships no GA: this module defines the
+semantics from SPEC and runs the generation loop on the device
+(``tv_ga_run``: one cooperative sm_100a kernel per call, fitness -> roulette
+CDF -> selection / crossover / Poisson mutation for every child).  The
+per-child random stream is counter-based splitmix64 keyed by (seed,
+generation, child), the same construction as the enumeration path
+(_k:38-60), so every trajectory is reproducible and independent of launch
+geometry; the CPU restatement oracle/tv_ga_oracle.c reproduces it bit for bit
+(tests/test_ga.py).  The single-genome operators below are host utilities
+with the same draw semantics (they are what one child of the kernel does).
+
+Genomes are held as the integer ``Genome.to_int()`` (genome bit 0 = most
+significant of L bits); L <= 64.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .genome import Genome, SearchSpace
+
+GOLD = 0x9E3779B97F4A7C15
+MIXA = 0xBF58476D1CE4E5B9
+MIXB = 0x94D049BB133111EB
+M64 = (1 << 64) - 1
+
+MODES = {"asexual": 0, "single_point": 1, "uniform": 2}
+
+
+def _mix64(z: int) -> int:
+    z = ((z ^ (z >> 30)) * MIXA) & M64
+    z = ((z ^ (z >> 27)) * MIXB) & M64
+    return z ^ (z >> 31)
+
+
+class GaRng:
+    """Counter-based stream of one child: key (seed, generation, child)."""
+
+    __slots__ = ("s",)
+
+    def __init__(self, seed: int, generation: int = 0, child: int = 0):
+        z = _mix64((seed ^ ((GOLD * (generation + 1)) & M64)) & M64)
+        self.s = _mix64(z ^ ((MIXA * (child + 1)) & M64))
+
+    def next(self) -> int:
+        self.s = (self.s + GOLD) & M64
+        return _mix64(self.s)
+
+    def below(self, n: int) -> int:
+        """((draw >> 32) * n) >> 32, the reference's bounded draw (_k:57-60)."""
+        return ((self.next() >> 32) * n) >> 32
+
+    def mulhi(self, n: int) -> int:
+        """uniform integer in [0, n) for any n < 2^64: high word of draw * n."""
+        return (self.next() * n) >> 64
+
+
+def poisson_thresholds(lam: float, L: int) -> np.ndarray:
+    """T[j] = floor(P(K <= j) * 2^63) for K ~ Poisson(lam), j < L (Eq. 1).
+
+    A flip count is k = #{j : (draw >> 1) >= T[j]}, i.e. inversion sampling
+    clamped at L (App. D.1 "if(r_fNrMutations > mBitLengthGenome)").  Computed
+    once on the host and shared by the device and the CPU restatement."""
+    if lam < 0:
+        raise ValueError("lambda must be >= 0")
+    T = np.empty(L, np.uint64)
+    p = math.exp(-lam)
+    cdf = 0.0
+    for j in range(L):
+        cdf += p
+        p *= lam / (j + 1)
+        T[j] = min(1 << 63, int(math.floor(min(cdf, 1.0) * 2.0 ** 63)))
+    return T
+
+
+# ---------------------------------------------------------------- single-genome operators
+def _as_int(g) -> tuple[int, int | None]:
+    return (g.to_int(), g.length) if isinstance(g, Genome) else (int(g), None)
+
+
+def poisson_sample(lam: float, rng: GaRng, L: int = 64) -> int:
+    """k ~ Poisson(lam) by inversion against poisson_thresholds (clamped to L)."""
+    T = poisson_thresholds(lam, L)
+    u = rng.next() >> 1
+    return int(np.count_nonzero(u >= T))
+
+
+def mutate(g, lam: float, rng: GaRng, L: int | None = None):
+    """Flip k ~ Poisson(lam) (clamped to L) DISTINCT uniform positions."""
+    v, glen = _as_int(g)
+    L = L or glen
+    k = poisson_sample(lam, rng, L)
+    chosen = 0
+    while bin(chosen).count("1") < k:
+        chosen |= 1 << (L - 1 - rng.below(L))
+    out = v ^ chosen
+    return Genome.from_int(L, out) if glen else out
+
+
+def crossover_single_point(a, b, rng: GaRng, L: int | None = None):
+    """Child = a's bits at positions < p, b's from p on; p uniform in [0, L)."""
+    av, la = _as_int(a)
+    bv, lb = _as_int(b)
+    if la is not None and la != lb:
+        raise ValueError("genome lengths differ")
+    L = L or la
+    p = rng.below(L)
+    full = (1 << L) - 1
+    top = 0 if p == 0 else full & ~((1 << (L - p)) - 1)
+    out = (av & top) | (bv & ~top & full)
+    return Genome.from_int(L, out) if la else out
+
+
+def crossover_uniform(a, b, rng: GaRng, L: int | None = None):
+    """Each bit from a or b with probability 1/2."""
+    av, la = _as_int(a)
+    bv, lb = _as_int(b)
+    if la is not None and la != lb:
+        raise ValueError("genome lengths differ")
+    L = L or la
+    m = rng.next() & ((1 << L) - 1)
+    out = (av & ~m) | (bv & m)
+    return Genome.from_int(L, out) if la else out
+
+
+def roulette_select(weights, rng: GaRng | None = None, cutoff=None) -> int:
+    """Smallest i whose partial sum reaches the draw (App. C.1).
+
+    With ``cutoff`` given it is the draw itself (weights {2,3,4,1}, cutoff 10 -> 3).
+    Otherwise integer weights use an exact integer draw r in [0, sum) and return
+    the first i with partial sum > r (= partial sum >= r + 1/2, so zero weights
+    are never picked); sum == 0 falls back to a uniform index."""
+    w = np.asarray(weights)
+    cs = np.cumsum(w)
+    if cutoff is not None:
+        return int(np.searchsorted(cs, cutoff, side="left"))
+    total = cs[-1]
+    if total <= 0:
+        return rng.mulhi(len(w))
+    if np.issubdtype(w.dtype, np.integer):
+        r = rng.mulhi(int(total))
+        return int(np.searchsorted(cs, r, side="right"))
+    u = (rng.next() >> 11) * 2.0 ** -53 * float(total)
+    return int(np.searchsorted(cs, u, side="right"))
+
+
+def fujiyama_fitness(g) -> int:
+    """Hamming weight."""
+    v, _ = _as_int(g)
+    return bin(v).count("1")
+
+
+# ---------------------------------------------------------------- run records
+@dataclass
+class GAConfig:
+    pop_size: int = 512
+    length: int = 32
+    mu_L: float = 0.3                  # lambda = expected flips per genome per generation
+    mode: str = "asexual"              # asexual | single_point | uniform
+    cutoff: int = 20000
+    target: int = 25                   # H >= 25 (Figs. 9-10)
+    adapt_fraction: float = 0.5        # half the population at target
+    stop_when: str = "adaptation"      # never | discovery | adaptation
+    init: np.ndarray | None = None     # u64 genomes; default all-zero
+
+
+@dataclass
+class RunRecord:
+    best: np.ndarray
+    mean: np.ndarray
+    count_at_target: np.ndarray
+    generations: int
+    discovery: int | None              # None = censored at the cutoff
+    adaptation: int | None
+    config: GAConfig = field(default=None)
+    seed: int = 0
+
+
+def discovery_time(record: RunRecord):
+    """First generation any individual met the target, or None (censored)."""
+    return record.discovery
+
+
+def adaptation_time(record: RunRecord, proportion: float | None = None, threshold: int | None = None):
+    """First generation >= proportion*N individuals met the threshold, or None (censored)."""
+    cfg = record.config
+    if threshold is not None and cfg is not None and threshold != cfg.target:
+        raise ValueError("counts were recorded for the configured target only")
+    x = cfg.adapt_fraction if proportion is None else proportion
+    need = math.ceil(x * cfg.pop_size)
+    hit = np.nonzero(record.count_at_target >= need)[0]
+    return int(hit[0]) if hit.size else None
+
+
+def bootstrap_median_ci(samples, sample_size: int = 100, resamples: int = 10000, rng=None, alpha: float = 0.05):
+    """Sample median and percentile CI of the bootstrap median distribution."""
+    x = np.asarray(samples, dtype=np.float64)
+    if x.size == 0:
+        raise ValueError("samples must be non-empty")
+    rng = rng if rng is not None else np.random.default_rng(0)
+    meds = np.median(x[rng.integers(0, x.size, (resamples, sample_size))], axis=1)
+    return float(np.median(x)), float(np.quantile(meds, alpha / 2)), float(np.quantile(meds, 1 - alpha / 2))
+
+
+# ---------------------------------------------------------------- device engine
+class DeviceGA:
+    """Device population + generation loop (tv_ga_*)."""
+
+    def __init__(self, pop_size: int, length: int, mu_L: float, mode: str = "asexual"):
+        self.n, self.L = int(pop_size), int(length)
+        self.mode = MODES[mode] if isinstance(mode, str) else int(mode)
+        self.T = poisson_thresholds(mu_L, self.L)
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().tv_ga_create(self.n, self.L, self.mode, _lib.ptr(self.T), ctypes.byref(h)))
+        self._h = h
+        self._fit = None
+
+    def close(self):
+        if self._h:
+            _lib.lib().tv_ga_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_population(self, genomes=None):
+        g = None if genomes is None else np.ascontiguousarray(genomes, np.uint64)
+        _lib.check(_lib.lib().tv_ga_set_population(self._h, _lib.ptr(g), None))
+
+    def population(self) -> np.ndarray:
+        out = np.empty(self.n, np.uint64)
+        _lib.check(_lib.lib().tv_ga_get_population(self._h, _lib.ptr(out), None))
+        return out
+
+    def run(self, seed: int, g0: int, n_gens: int, target: int, adapt_count: int, stop_when: int,
+            f_ext=None):
+        best = np.zeros(n_gens, np.uint32)
+        sm = np.zeros(n_gens, np.uint64)
+        cnt = np.zeros(n_gens, np.uint32)
+        done = ctypes.c_int64()
+        _lib.check(_lib.lib().tv_ga_run(self._h, int(np.uint64(seed)), int(g0), int(n_gens), int(target),
+                                        int(adapt_count), int(stop_when), _lib.ptr(f_ext), _lib.ptr(best),
+                                        _lib.ptr(sm), _lib.ptr(cnt), ctypes.byref(done), None))
+        k = done.value
+        return k, best[:k], sm[:k], cnt[:k]
+
+    def jatam_fitness(self, space: SearchSpace, target_occ: np.ndarray, d: int = 19, k: int = 8, seed: int = 0,
+                      strict: bool = True):
+        """Device vector of JaTAM-shape fitness for the current population (enumeration indices)."""
+        import torch
+        if self._fit is None:
+            self._fit = torch.empty(self.n, dtype=torch.int32, device="cuda")
+        a, bpl, mp, mv, fp = space.kernel_args()
+        occ = np.ascontiguousarray(np.asarray(target_occ, dtype=bool).reshape(d * d), np.uint8)
+        _lib.check(_lib.lib().tv_ga_fitness_jatam(self._h, a, bpl, _lib.ptr(mp), _lib.ptr(mv), mp.shape[0],
+                                                  _lib.ptr(fp), fp.shape[0], d, k, int(np.uint64(seed)),
+                                                  int(bool(strict)), _lib.ptr(occ), _lib.ptr(self._fit), None))
+        return self._fit
+
+
+@dataclass
+class JatamFitness:
+    """GA fitness 'evolve toward a target shape' (SPEC:454 leaves it open):
+    for a genome DETERMINISTIC at k, d^2 - shapediff(target, run-0 grid) with both
+    grids seed-centred (App. B.2 shapesim scaled by d^2); otherwise 0."""
+
+    space: SearchSpace
+    target_occ: np.ndarray  # bool (d, d)
+    d: int = 19
+    k: int = 8
+    seed: int = 0
+    strict: bool = True
+
+
+def run_ga(cfg: GAConfig, fitness="fujiyama", seed: int = 0, chunk: int = 4096) -> RunRecord:
+    """Generation loop on the device: evaluate, record, stop when the
+    configured target is met (or at the cutoff), reproduce with full replacement."""
+    jatam = isinstance(fitness, JatamFitness)
+    if not jatam and fitness != "fujiyama":
+        raise ValueError("fitness must be 'fujiyama' or a JatamFitness")
+    if jatam and fitness.space.free_bit_count != cfg.length:
+        raise ValueError("GA genome length must equal the space's free bit count")
+    ga = DeviceGA(cfg.pop_size, cfg.length, cfg.mu_L, cfg.mode)
+    try:
+        if cfg.init is not None:
+            ga.set_population(cfg.init)
+        adapt_count = math.ceil(cfg.adapt_fraction * cfg.pop_size)
+        stop = {"never": 0, "discovery": 1, "adaptation": 2}[cfg.stop_when]
+        bests, sums, cnts = [], [], []
+        g = 0
+        while g < cfg.cutoff:
+            if jatam:
+                f = ga.jatam_fitness(fitness.space, fitness.target_occ, fitness.d, fitness.k, fitness.seed,
+                                     fitness.strict)
+                k, b, s, c = ga.run(seed, g, 1, cfg.target, adapt_count, stop, f_ext=f)
+            else:
+                k, b, s, c = ga.run(seed, g, min(chunk, cfg.cutoff - g), cfg.target, adapt_count, stop)
+            bests.append(b); sums.append(s); cnts.append(c)
+            g += k
+            if stop and c.size and ((stop == 1 and c[-1] >= 1) or (stop == 2 and c[-1] >= adapt_count)):
+                break
+    finally:
+        ga.close()
+    best = np.concatenate(bests) if bests else np.zeros(0, np.uint32)
+    cnt = np.concatenate(cnts) if cnts else np.zeros(0, np.uint32)
+    mean = (np.concatenate(sums).astype(np.float64) / cfg.pop_size) if sums else np.zeros(0)
+    disc = np.nonzero(cnt >= 1)[0]
+    adap = np.nonzero(cnt >= adapt_count)[0]
+    return RunRecord(best, mean, cnt, int(best.size), int(disc[0]) if disc.size else None,
+                     int(adap[0]) if adap.size else None, cfg, seed)
+
+
+def sweep(mu_L_grid, runs: int = 100, base: GAConfig | None = None, seed0: int = 0, sample_size: int = 100,
+          resamples: int = 10000) -> list[dict]:
+    """SPEC:452 sweep JSON rows: {muL, runs, discovery:{median, ci_lo, ci_hi, censored}, adaptation:{...}}."""
+    base = base or GAConfig()
+    rows = []
+    for mu in mu_L_grid:
+        cfg = GAConfig(**{**base.__dict__, "mu_L": float(mu)})
+        recs = [run_ga(cfg, seed=seed0 + r) for r in range(runs)]
+        row = {"muL": float(mu), "runs": runs}
+        for name, vals in (("discovery", [r.discovery for r in recs]), ("adaptation", [r.adaptation for r in recs])):
+            ok = [v for v in vals if v is not None]
+            cens = len(vals) - len(ok)
+            if ok and cens * 2 <= len(vals):
+                med, lo, hi = bootstrap_median_ci(ok, sample_size, resamples)
+                row[name] = dict(median=med, ci_lo=lo, ci_hi=hi, censored=cens)
+            else:
+                row[name] = dict(median=None, ci_lo=None, ci_hi=None, censored=cens)
+        rows.append(row)
+    return rows

@@ -1,0 +1,204 @@
+"""GA (SPEC.md evolve module).  No reference implementation exists, so:
+ * the device loop must equal the CPU restatement (oracle/tv_ga_oracle.c) bit
+   for bit (gpu tests), and the host single-genome operators must equal the
+   restatement's child procedure (cpu tests);
+ * the operators must meet SPEC.md's statistical acceptance (ACCEPTANCE 4-5).
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2205_15311_b200 import evolve as E
+from paper_2205_15311_b200.genome import Genome
+
+
+def test_stream_matches_restatement():
+    for seed, g, i in [(0, 0, 0), (7, 3, 11), (2**63 + 5, 19999, 2**20 - 1)]:
+        r = E.GaRng(seed, g, i)
+        assert [r.next() for _ in range(8)] == [int(x) for x in O.ga_draws(seed, g, i, 8)]
+
+
+def _py_child(seed, g, i, pop, L, mode, T):
+    """One child composed from the host operators (same draw order as the kernel)."""
+    r = E.GaRng(seed, g, i)
+    w = np.array([bin(int(v)).count("1") for v in pop], np.int64)
+    a = int(pop[E.roulette_select(w, r)])
+    child = a
+    if mode:
+        b = int(pop[E.roulette_select(w, r)])
+        child = E.crossover_single_point(a, b, r, L) if mode == 1 else E.crossover_uniform(a, b, r, L)
+    u = r.next() >> 1
+    k = int(np.count_nonzero(u >= T))
+    chosen = 0
+    while bin(chosen).count("1") < k:
+        chosen |= 1 << (L - 1 - r.below(L))
+    return child ^ chosen
+
+
+@pytest.mark.parametrize("mode,lam,L", [(0, 0.3, 32), (1, 1.0, 24), (2, 4.0, 64), (1, 0.0, 16)])
+def test_host_operators_equal_restatement(mode, lam, L):
+    rng = np.random.default_rng(mode * 10 + L)
+    full = (1 << L) - 1
+    pop = np.array([int(x) & full for x in rng.integers(0, 2**63, 37, dtype=np.uint64)], np.uint64)
+    pop[::5] = 0
+    cdf = np.cumsum([bin(int(v)).count("1") for v in pop]).astype(np.uint64)
+    T = E.poisson_thresholds(lam, L)
+    for i in range(40):
+        assert _py_child(9, 4, i, pop, L, mode, T) == O.ga_child(9, 4, i, pop, cdf, L, mode, T)
+
+
+def test_zero_fitness_falls_back_to_uniform():
+    pop = np.zeros(8, np.uint64)
+    cdf = np.zeros(8, np.uint64)
+    T = E.poisson_thresholds(0.0, 32)
+    assert all(O.ga_child(1, 0, i, pop, cdf, 32, 0, T) == 0 for i in range(50))
+
+
+def test_mutation_properties():
+    T0 = E.poisson_thresholds(0.0, 32)
+    assert not T0.any() or (T0 == 1 << 63).all()
+    g = Genome.from_int(32, 0xDEADBEEF)
+    for i in range(200):
+        assert E.mutate(g, 0.0, E.GaRng(1, 0, i)) == g
+    for i in range(2000):
+        r = E.GaRng(2, 0, i)
+        r2 = E.GaRng(2, 0, i)
+        k = E.poisson_sample(2.5, r2, 32)
+        m = E.mutate(0, 2.5, r, 32)
+        assert bin(m).count("1") == k                                           # distinct flips
+
+
+@pytest.mark.parametrize("lam", [0.1, 0.5, 1.0])
+def test_flip_count_distribution_chi2(lam):
+    """SPEC ACCEPTANCE 5: chi^2 against Eq. 1 truncated at L, p > 0.001, 10^6 draws."""
+    from scipy import stats
+    L = 32
+    ks = O.ga_flip_counts(12345, 10**6, L, E.poisson_thresholds(lam, L))
+    kmax = 1
+    while stats.poisson.sf(kmax, lam) * 1e6 > 5:
+        kmax += 1
+    obs = np.array([np.count_nonzero(ks == j) for j in range(kmax)] + [np.count_nonzero(ks >= kmax)], float)
+    p = np.array([stats.poisson.pmf(j, lam) for j in range(kmax)] + [stats.poisson.sf(kmax - 1, lam)])
+    assert stats.chisquare(obs, p * obs.sum()).pvalue > 0.001
+    assert abs(ks.mean() - lam) < 5 * math.sqrt(lam / 1e6)
+
+
+def test_roulette_known_answers():
+    assert E.roulette_select([2.0, 3.0, 4.0, 1.0], cutoff=10) == 3             # App. C.1
+    assert all(E.roulette_select([1, 0, 0], E.GaRng(0, 0, i)) == 0 for i in range(200))
+
+
+def test_selection_frequencies_3sigma():
+    """10^6 children of one asexual, lambda = 0 generation: parent frequencies ~ f_i / sum f (SPEC ACCEPTANCE 5)."""
+    n = 1 << 20
+    pat = np.array([0b1, 0b11, 0b111, 0b1111], np.uint64)                      # fitness 1, 2, 3, 4
+    pop = np.tile(pat, n // 4)
+    O.ga_run(pop, 32, 0, E.poisson_thresholds(0.0, 32), 5, 0, 1, 32, 1 << 30, 0)
+    cnt = np.array([np.count_nonzero(pop == v) for v in pat], float)
+    p = np.array([1, 2, 3, 4]) / 10.0
+    assert np.all(np.abs(cnt - n * p) <= 3 * np.sqrt(n * p * (1 - p)))
+
+
+def test_uniform_crossover_and_single_point_properties():
+    L = 32
+    full = (1 << L) - 1
+    hw = []
+    for i in range(20000):
+        r = E.GaRng(3, 0, i)
+        c = E.crossover_uniform(0, full, r, L)
+        hw.append(bin(c).count("1"))
+    hw = np.array(hw)
+    assert abs(hw.mean() - L / 2) < 3 * math.sqrt(L / 4 / len(hw)) * 3
+    for i in range(2000):
+        a, b = 0x0F0F0F0F, 0xF0F0F0F0
+        c = E.crossover_single_point(a, b, E.GaRng(4, 0, i), L)
+        assert all(((c >> j) & 1) in (((a >> j) & 1), ((b >> j) & 1)) for j in range(L))
+    # p = 0 -> child == b: find a stream whose first draw gives p = 0
+    for i in range(10**5):
+        r = E.GaRng(5, 0, i)
+        if E.GaRng(5, 0, i).below(L) == 0:
+            assert E.crossover_single_point(a, b, r, L) == b
+            break
+
+
+def test_bootstrap_examples():
+    assert E.bootstrap_median_ci([5, 5, 5], 3, 100) == (5.0, 5.0, 5.0)
+    med, lo, hi = E.bootstrap_median_ci(np.arange(1, 101), 100, 2000)
+    assert med == 50.5 and lo < 50.5 < hi and hi - lo < 25
+    with pytest.raises(ValueError):
+        E.bootstrap_median_ci([], 10, 10)
+
+
+# ---------------------------------------------------------------- device (gpu)
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,L,mode,lam,stop", [(512, 32, 0, 0.3, 0), (4096 + 3, 32, 1, 1.0, 0), (1 << 16, 64, 2, 4.0, 0),
+                                                 (1000, 24, 0, 0.03, 2), (1 << 20, 32, 0, 0.3, 0)])
+def test_device_ga_equals_restatement(n, L, mode, lam, stop):
+    ga = E.DeviceGA(n, L, lam, mode)
+    init = np.random.default_rng(n).integers(0, 2**63, n, dtype=np.uint64) & np.uint64((1 << L) - 1 if L < 64 else 2**64 - 1)
+    init[: n // 2] = 0
+    ga.set_population(init)
+    pop = init.copy()
+    T = E.poisson_thresholds(lam, L)
+    gens = 40 if n >= 1 << 20 else 300
+    tgt, adapt = 25, n // 2
+    g = 0
+    while g < gens:  # several launches continue the same trajectory
+        k, b, s, c = ga.run(11, g, min(97, gens - g), tgt, adapt, stop)
+        k2, b2, s2, c2 = O.ga_run(pop, L, mode, T, 11, g, min(97, gens - g), tgt, adapt, stop)
+        assert k == k2
+        assert np.array_equal(b, b2) and np.array_equal(s, s2) and np.array_equal(c, c2)
+        assert np.array_equal(ga.population(), pop), g
+        g += k
+        if stop and k < min(97, gens - g + k):
+            break
+    ga.close()
+
+
+@pytest.mark.gpu
+def test_fujiyama_regime_desk_scale():
+    """SPEC ACCEPTANCE 4 (runs=25, pop=512, L=32, cutoff=20000)."""
+    med = []
+    for mu in (0.03, 0.1, 0.3):
+        d = [E.run_ga(E.GAConfig(mu_L=mu, stop_when="discovery"), seed=r).discovery for r in range(25)]
+        d = [x if x is not None else 20000 for x in d]
+        med.append(np.median(d))
+    assert med[0] > med[1] > med[2], med
+    ok03 = sum(E.run_ga(E.GAConfig(mu_L=0.3), seed=100 + r).adaptation is not None for r in range(25))
+    cens4 = sum(E.run_ga(E.GAConfig(mu_L=4.0), seed=200 + r).adaptation is None for r in range(25))
+    assert ok03 >= 20 and cens4 >= 20, (ok03, cens4)
+
+
+@pytest.mark.gpu
+def test_jatam_fitness_matches_cpu():
+    """Device JaTAM-shape fitness == d^2 - shapediff(target, run-0 grid) for DET genomes (oracle)."""
+    from paper_2205_15311_b200._kernels import edges_from_labels
+    from paper_2205_15311_b200.genome import SearchSpace, decode_tileset, genome_at_index
+    S28 = SearchSpace(2, 8)
+    d, k = 19, 8
+    # target: the run-0 grid of a 12-cell deterministic genome
+    tgt_idx = 0x801772
+    ts = decode_tileset(genome_at_index(S28, tgt_idx), S28)
+    e = edges_from_labels(np.array([v for t in ts.tiles for v in t], np.uint8), 2)
+    grid = np.empty(d * d, np.int16)
+    O.assemble_single(e, 2, d, 0, tgt_idx, 0, True, grid)
+    target = (grid >= 0).reshape(d, d)
+    n = 4096
+    pop = np.random.default_rng(3).integers(0, 1 << 24, n, dtype=np.uint64)
+    ga = E.DeviceGA(n, 24, 0.3)
+    ga.set_population(pop)
+    f = ga.jatam_fitness(S28, target, d, k).cpu().numpy().view(np.uint32)
+    for i in range(n):
+        idx = int(pop[i])
+        ts = decode_tileset(genome_at_index(S28, idx), S28)
+        e = edges_from_labels(np.array([v for t in ts.tiles for v in t], np.uint8), 2)
+        sw = np.zeros(6, np.uint64)
+        st, cls, *_ = O.classify_single(e, 2, d, k, 0, idx, True, sw)
+        exp = 0
+        if st == 0 and cls == 0:
+            O.assemble_single(e, 2, d, 0, idx, 0, True, grid)
+            exp = d * d - int(np.count_nonzero((grid >= 0).reshape(d, d) != target))
+        assert int(f[i]) == exp, (i, idx)
+    ga.close()
