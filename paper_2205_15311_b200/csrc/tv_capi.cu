@@ -661,12 +661,7 @@ int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **
   GaParams &P = h->P;
   P.n = n; P.L = L; P.mode = mode;
   for (int j = 0; j < 64; j++) P.T[j] = j < L ? T[j] : ~0ULL;
-  P.seg = 32;
-  P.seg_shift = 5;
-  while (P.seg * 32768 < n) { P.seg <<= 1; P.seg_shift++; }
-  P.n_coarse = (n + P.seg - 1) / P.seg;
-  h->smem = (size_t)P.n_coarse * 4;
-  CK(cudaFuncSetAttribute((const void *)k_ga_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem));
+  h->smem = 0;
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ga_run, 1024, h->smem));
   if (per_sm < 1) { delete h; return fail(TV_ERR_CUDA, "GA kernel does not fit one CTA per SM"); }
@@ -678,7 +673,8 @@ int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **
   e = e ? e : cudaMalloc(&P.pop0, n * 8);
   e = e ? e : cudaMalloc(&P.pop1, n * 8);
   e = e ? e : cudaMalloc(&P.cdf, n * 4);
-  e = e ? e : cudaMalloc(&P.coarse, P.n_coarse * 4);
+  e = e ? e : cudaMalloc(&P.guide, n * 4);
+  e = e ? e : cudaMalloc(&P.fstage, n * 4);
   e = e ? e : cudaMalloc(&P.tot, (size_t)h->nblocks * 8);
   e = e ? e : cudaMalloc(&P.done, 8);
   e = e ? e : cudaMalloc(&P.final_buf, 4);
@@ -691,7 +687,7 @@ int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **
 int tv_ga_destroy(tv_ga *h) {
   if (!h) return 0;
   GaParams &P = h->P;
-  cudaFree(P.pop0); cudaFree(P.pop1); cudaFree(P.cdf); cudaFree(P.coarse); cudaFree(P.tot);
+  cudaFree(P.pop0); cudaFree(P.pop1); cudaFree(P.cdf); cudaFree(P.guide); cudaFree(P.fstage); cudaFree(P.tot);
   cudaFree(P.done); cudaFree(P.final_buf);
   delete h;
   return 0;

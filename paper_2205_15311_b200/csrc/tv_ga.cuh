@@ -1,15 +1,22 @@
 // tv_ga.cuh -- GA generation loop (SPEC.md evolve module).
 //
 // One cooperative persistent kernel runs many generations; per generation:
-//   A. fitness (Fujiyama popcount, or an externally computed vector), per
-//      thread sums over a contiguous run, a block scan, and the stats;
-//   B. grid barrier; chunk offsets -> global inclusive CDF (u32) and a coarse
-//      table (last CDF value of every s-entry segment, <= 32768 entries);
-//   C. grid barrier; every CTA stages the coarse table in shared memory and
-//      produces its chunk of children: roulette selection = search of the
-//      coarse table in shared memory + a binary search inside one s-entry
-//      segment (one cache line for s = 32), crossover, Poisson mutation;
-//   D. grid barrier; swap population buffers.
+//   A. per-thread sums over a contiguous run of the fitness vector (staged in
+//      index order when the children were made), block scan, stats;
+//   -- grid barrier --
+//   B. chunk offsets -> global inclusive CDF (u32) and a guide table for
+//      indexed search (Chen & Asau): the r-range [0, total) is cut into
+//      B = min(n, total) monotone buckets b(r) = (r * M) >> 32 and guide[b] =
+//      the individual owning the first r of bucket b; individual j writes the
+//      buckets whose first r lies in its own range [cdf[j-1], cdf[j]), so the
+//      table is built in the same pass;
+//   -- grid barrier --
+//   C. children: all random draws of a child first (selection draws,
+//      crossover mask, mutation mask), then selection = guide[b(r)] plus a short
+//      forward scan while cdf[j] <= r (exactly the first j with cdf[j] > r),
+//      parent loads and the child, two children interleaved per thread; the
+//      child's Fujiyama fitness is staged for the next generation's phase A.
+// Two grid barriers per generation.
 // Data written by other CTAs is read only after a grid barrier (grid.sync()
 // orders and publishes all prior writes of the grid; its gpu-scope acquire
 // invalidates L1), so ordinary cached loads are used.
@@ -33,14 +40,12 @@ struct GaParams {
   uint64_t seed;
   int64_t g0, n_gens;
   int64_t chunk;         // individuals per CTA (contiguous)
-  int64_t seg;           // coarse segment length s (power of two)
-  int32_t seg_shift;     // log2(seg)
-  int64_t n_coarse;      // ceil(n / seg)
   uint64_t T[64];        // Poisson CDF thresholds x 2^63 (k = #{j < L : (draw >> 1) >= T[j]})
   unsigned long long *pop0, *pop1;
   const uint32_t *f_ext;
   uint32_t *cdf;         // n
-  uint32_t *coarse;      // n_coarse
+  uint32_t *fstage;      // n: fitness staged in index order (own chunk per CTA)
+  uint32_t *guide;       // n (first B entries used in a generation)
   unsigned long long *tot;  // per CTA chunk totals
   uint32_t *best;        // n_gens
   unsigned long long *sum;  // n_gens
@@ -57,41 +62,33 @@ __device__ __forceinline__ uint32_t ga_below(uint64_t &s, uint32_t n) {
   return (uint32_t)(((ga_draw(s) >> 32) * (uint64_t)n) >> 32);
 }
 
-// roulette selection: first j with cdf[j] > r, r = mulhi(draw, total)
-__device__ __forceinline__ int64_t ga_select(uint64_t &s, const GaParams &P, const uint32_t *coarse_s,
-                                             uint32_t total) {
-  const uint64_t x = ga_draw(s);
-  if (total == 0) return (int64_t)__umul64hi(x, (uint64_t)P.n);  // SPEC:447 uniform fallback
-  const uint32_t r = (uint32_t)__umul64hi(x, (uint64_t)total);
-  int64_t lo = 0, hi = P.n_coarse - 1;  // first segment whose last value exceeds r
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (coarse_s[mid] > r) hi = mid; else lo = mid + 1;
-  }
-  int64_t a = lo << P.seg_shift, b = min(P.n, a + P.seg) - 1;
-  while (a < b) {
-    const int64_t mid = (a + b) >> 1;
-    if (P.cdf[mid] > r) b = mid; else a = mid + 1;  // one 128-B line for seg = 32: L1 after the first probe
-  }
-  return a;
-}
+// Draw-side of one child: everything that depends only on its random stream
+// (draw order fixed by oracle/tv_ga_oracle.c): the two roulette draws, the
+// crossover mask and the mutation mask.  The memory-dependent part (guide
+// lookup, CDF scan, parent loads) is done afterwards for several children at
+// once so their L2 latencies overlap.
+struct ChildDraws {
+  uint32_t ra, rb;      // roulette draws in [0, total) (or uniform indices when total == 0)
+  uint64_t top;         // crossover: bits taken from parent a (mode 1); uniform: mask of bits from b (mode 2)
+  uint64_t flips;       // mutation mask
+};
 
-__device__ __forceinline__ uint64_t ga_child(const GaParams &P, const unsigned long long *pop, int64_t g,
-                                             int64_t i, const uint32_t *coarse_s, uint32_t total) {
-  uint64_t s = stream_state(P.seed, (uint64_t)g, (uint64_t)i);
+__device__ __forceinline__ ChildDraws ga_draws(const GaParams &P, uint64_t gkey, int64_t i, uint32_t total) {
+  ChildDraws D;
+  uint64_t s = mix64(gkey ^ (kMixA * ((uint64_t)i + 1)));  // = stream_state(seed, g, i), gkey hoisted
   const int L = P.L;
   const uint64_t full = L == 64 ? ~0ULL : ((1ULL << L) - 1);
-  const uint64_t a = pop[ga_select(s, P, coarse_s, total)];
-  uint64_t child = a;
+  const uint64_t range = total ? (uint64_t)total : (uint64_t)P.n;  // SPEC:447 uniform fallback
+  D.ra = (uint32_t)__umul64hi(ga_draw(s), range);
+  D.rb = 0;
+  D.top = full;
   if (P.mode != 0) {
-    const uint64_t b = pop[ga_select(s, P, coarse_s, total)];
+    D.rb = (uint32_t)__umul64hi(ga_draw(s), range);
     if (P.mode == 1) {  // positions < p from a, >= p from b
       const uint32_t p = ga_below(s, (uint32_t)L);
-      const uint64_t top = p == 0 ? 0ULL : (full & ~((1ULL << (L - p)) - 1));
-      child = (a & top) | (b & ~top & full);
+      D.top = p == 0 ? 0ULL : (full & ~((1ULL << (L - p)) - 1));
     } else {            // each bit from b where the mask is set
-      const uint64_t m = ga_draw(s) & full;
-      child = (a & ~m) | (b & m);
+      D.top = full & ~ga_draw(s);
     }
   }
   const uint64_t u = ga_draw(s) >> 1;  // k ~ Poisson(lambda) clamped to L
@@ -105,13 +102,21 @@ __device__ __forceinline__ uint64_t ga_child(const GaParams &P, const unsigned l
     chosen |= bit;
     f++;
   }
-  return (child ^ chosen) & full;
+  D.flips = chosen;
+  return D;
+}
+
+// roulette: first j with cdf[j] > r, from the guide entry of r's bucket
+__device__ __forceinline__ uint32_t ga_pick(const GaParams &P, uint32_t r, uint32_t total, uint64_t mul) {
+  if (total == 0) return r;
+  uint32_t j = P.guide[(uint32_t)(((uint64_t)r * mul) >> 32)];  // mul <= 2^32: no overflow
+  while (P.cdf[j] <= r) j++;
+  return j;
 }
 
 __global__ void __launch_bounds__(1024, 1) k_ga_run(const __grid_constant__ GaParams P) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
-  extern __shared__ uint32_t coarse_s[];       // n_coarse
   __shared__ uint32_t warp_sum[32];
   __shared__ uint32_t s_best, s_cnt;
   __shared__ unsigned long long s_off, s_total;
@@ -124,15 +129,19 @@ __global__ void __launch_bounds__(1024, 1) k_ga_run(const __grid_constant__ GaPa
   const int64_t i0 = c0 + tid * per, i1 = min(c1, i0 + per);
   int cur = 0;
   int64_t t = 0;
+  // fitness of the initial population, staged in index order
+  for (int64_t i = c0 + tid; i < c1; i += nt)
+    P.fstage[i] = P.fitness == 0 ? (uint32_t)__popcll(P.pop0[i]) : P.f_ext[i];
+  __syncthreads();
   for (; t < P.n_gens; t++) {
     const int64_t g = P.g0 + t;
     const unsigned long long *pop = cur ? P.pop1 : P.pop0;
     unsigned long long *nxt = cur ? P.pop0 : P.pop1;
     if (tid == 0) { s_best = 0; s_cnt = 0; }
-    // ---- A: fitness sums per thread, block scan -> thread offsets, stats
+    // ---- A: per-thread sums over a contiguous run of staged fitness, block scan, stats
     uint32_t acc = 0, best = 0, cnt = 0;
     for (int64_t i = i0; i < i1; i++) {
-      const uint32_t f = P.fitness == 0 ? (uint32_t)__popcll(pop[i]) : P.f_ext[i];
+      const uint32_t f = P.fstage[i];
       acc += f;
       best = max(best, f);
       cnt += f >= P.target;
@@ -169,11 +178,11 @@ __global__ void __launch_bounds__(1024, 1) k_ga_run(const __grid_constant__ GaPa
       atomicAdd(&P.count[t], s_cnt);
     }
     grid.sync();
-    // ---- B: chunk offsets -> global CDF + coarse table; stop decision
+    // ---- B: chunk offsets -> global CDF + guide table; stop decision
     if (wid == 0) {
       unsigned long long o = 0, tt = 0;
       for (int j = lane; j < (int)gridDim.x; j += 32) {
-        const unsigned long long v = __ldcg(&P.tot[j]);
+        const unsigned long long v = P.tot[j];
         tt += v;
         if (j < (int)blockIdx.x) o += v;
       }
@@ -191,23 +200,53 @@ __global__ void __launch_bounds__(1024, 1) k_ga_run(const __grid_constant__ GaPa
     }
     __syncthreads();
     const uint32_t total = (uint32_t)s_total;
+    // bucket function b(r) = (r * mul) >> 32, monotone, B = min(n, total) buckets
+    const uint64_t nb = min((uint64_t)P.n, (uint64_t)total);
+    const uint64_t mul = total ? (nb << 32) / total : 0ull;
     if (blockIdx.x == 0 && tid == 0) P.sum[t] = s_total;
     if (s_stop) { t++; break; }
     {
-      uint32_t run = (uint32_t)s_off + excl;
+      uint32_t prev = (uint32_t)s_off + excl, run = prev;
       for (int64_t i = i0; i < i1; i++) {
-        run += P.fitness == 0 ? (uint32_t)__popcll(pop[i]) : P.f_ext[i];
+        run += P.fstage[i];
         P.cdf[i] = run;
-        if (((i + 1) & (P.seg - 1)) == 0 || i == P.n - 1) P.coarse[i >> P.seg_shift] = run;
+        if (run != prev) {  // own r in [prev, run): buckets whose first r falls in it
+          const int64_t b0 = prev ? (int64_t)(((uint64_t)(prev - 1) * mul) >> 32) + 1 : 0;
+          const int64_t b1 = (int64_t)(((uint64_t)(run - 1) * mul) >> 32);
+          for (int64_t b = b0; b <= b1; b++) P.guide[b] = (uint32_t)i;
+        }
+        prev = run;
       }
     }
     grid.sync();
-    // ---- C: children
-    for (int64_t j = tid; j < P.n_coarse; j += nt) coarse_s[j] = P.coarse[j];
-    __syncthreads();
-    for (int64_t i = c0 + tid; i < c1; i += nt) nxt[i] = ga_child(P, pop, g, i, coarse_s, total);
+    const uint64_t gkey = mix64(P.seed ^ (kGold * ((uint64_t)g + 1)));  // stream_state prefix (_k:45-48)
+    // ---- C: children, two at a time (draws first, then the dependent loads);
+    //      the next generation's fitness is staged as the children are made
+    for (int64_t i = c0 + tid; i < c1; i += 2 * nt) {
+      const int64_t i2 = i + nt;
+      const bool two = i2 < c1;
+      const ChildDraws D1 = ga_draws(P, gkey, i, total);
+      const ChildDraws D2 = two ? ga_draws(P, gkey, i2, total) : D1;
+      const uint32_t a1 = ga_pick(P, D1.ra, total, mul), a2 = ga_pick(P, D2.ra, total, mul);
+      uint64_t c1v = pop[a1], c2v = pop[a2];
+      if (P.mode != 0) {
+        const uint32_t b1 = ga_pick(P, D1.rb, total, mul), b2 = ga_pick(P, D2.rb, total, mul);
+        const uint64_t p1 = pop[b1], p2 = pop[b2];
+        c1v = (c1v & D1.top) | (p1 & ~D1.top);
+        c2v = (c2v & D2.top) | (p2 & ~D2.top);
+      }
+      const uint64_t full = P.L == 64 ? ~0ULL : ((1ULL << P.L) - 1);
+      c1v = (c1v ^ D1.flips) & full;
+      nxt[i] = c1v;
+      if (P.fitness == 0) P.fstage[i] = (uint32_t)__popcll(c1v);
+      if (two) {
+        c2v = (c2v ^ D2.flips) & full;
+        nxt[i2] = c2v;
+        if (P.fitness == 0) P.fstage[i2] = (uint32_t)__popcll(c2v);
+      }
+    }
     cur ^= 1;
-    grid.sync();
+    __syncthreads();  // this CTA's staged fitness is read in index order by phase A
   }
   if (blockIdx.x == 0 && tid == 0) {
     *P.done = (unsigned long long)t;
