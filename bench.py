@@ -167,6 +167,54 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+def hbm_peak() -> float:
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0  # B200_PROFILING.md fallback
+
+
+def ga_bench(args, n: int = 1 << 20, gens: int = 2000) -> dict:
+    """GA generations/s at population 2^20 (BASELINE.json configs[2]): Fujiyama, L=32,
+    mu*L=0.3, asexual, no early stop; one cooperative launch per call."""
+    import torch
+    from oracle import oracle as O
+    from paper_2205_15311_b200 import evolve as E
+    dga = E.DeviceGA(n, 32, 0.3, "asexual")
+    dga.run(7, 0, 50, 25, n, 0)  # warm-up
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    k, best, sm, cnt = dga.run(7, 50, gens, 25, n, 0)
+    e1.record()
+    torch.cuda.synchronize()
+    dev_s = e0.elapsed_time(e1) / 1e3
+    dga.close()
+    # e2e: the public API (host call -> device loop -> per-generation records on the host)
+    t = time.perf_counter()
+    rec = E.run_ga(E.GAConfig(pop_size=n, length=32, mu_L=0.3, cutoff=gens, stop_when="never"), seed=7)
+    e2e_s = time.perf_counter() - t
+    # CPU restatement on all host threads (not a reference: none exists)
+    pop = np.zeros(n, np.uint64)
+    O.ga_run(pop, 32, 0, E.poisson_thresholds(0.3, 32), 7, 0, 1, 25, n, 0)
+    t = time.perf_counter()
+    cg = 3
+    O.ga_run(pop, 32, 0, E.poisson_thresholds(0.3, 32), 7, 1, cg, 25, n, 0)
+    cpu_s = time.perf_counter() - t
+    return {"metric": "GA generations/sec", "value": k / dev_s, "unit": "generations/s",
+            "config": {"workload": "Fujiyama GA, population 2^20, L=32, muL=0.3, asexual, roulette, no early stop",
+                       "generations_timed": int(k)},
+            "us_per_generation": dev_s / k * 1e6,
+            "e2e": {"value": rec.generations / e2e_s, "unit": "generations/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 16, "api": "evolve.run_ga"},
+            "roofline": {"bound": "hbm", "achieved": 16.0 * n * k / dev_s / 1e9, "peak": hbm_peak(), "unit": "GB/s",
+                         "frac": 16.0 * n * k / dev_s / 1e9 / hbm_peak(),
+                         "note": "16 B/individual/generation algorithmic (SURVEY 8d); working set L2-resident"},
+            "cpu_baseline": {"value": cg / cpu_s, "unit": "generations/s", "cores": os.cpu_count(),
+                             "kind": "restatement (no reference GA exists)",
+                             "sample": f"{cg} generations of 2^20 on oracle/tv_ga_oracle.c, OpenMP"}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -174,6 +222,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ga", action="store_true")
     args = ap.parse_args()
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
@@ -312,6 +361,9 @@ def main():
             cpu = cpu_port_rate()
         except Exception as e:  # the oracle is test infrastructure; report, do not fail the bench
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {e}"}
+    ga = None
+    if rank == 0 and not args.no_ga:
+        ga = ga_bench(args)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
@@ -324,7 +376,7 @@ def main():
                 "e2e": {"value": N_S28 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                         "d2h_bytes_per_step": int(d2h), "api": "classify.enumerate_space"},
                 "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(),
-                "gpu_launches": 2 * args.steps}
+                "gpu_launches": 2 * args.steps, "ga": ga}
         print(json.dumps(line), flush=True)
     hist.close()
     if world > 1:

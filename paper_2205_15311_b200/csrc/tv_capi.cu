@@ -177,14 +177,20 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
   if (C.fast) {
     const int PD = d + 2;
     P.GW = (PD * PD + 7) / 8;
-    const char *es = getenv("TV_STACK_S");
-    P.S = std::min(es ? std::max(4, atoi(es)) & ~1 : 64, (dd + 1) & ~1);
-    const char *et = getenv("TV_SERVICE_THRESH");
+    // tunables (env overrides exist for A/B measurements only)
+    const char *es = getenv("TV_STACK_S"), *ec = getenv("TV_CTA_SLOTS"), *et = getenv("TV_SERVICE_THRESH");
+    const char *eth = getenv("TV_FAST_THREADS");
     P.service_thresh = et ? atoi(et) : 0;
-    if (P.S < 4) P.S = 4;
+    P.cta_slots = P.hist_mode ? (ec ? atoi(ec) : 128) : 0;
+    int threads = eth ? std::min(atoi(eth), TV_FAST_MAXT) & ~31 : TV_FAST_MAXT;
+    if (es) {
+      P.S = std::max(4, atoi(es)) & ~1;
+    } else {  // largest shared movelist part (<= 64 entries) that keeps two CTAs per SM
+      P.S = 64;
+      while (P.S > 16 && 2 * (fast_smem_bytes(threads, P.GW, P.S, P.cta_slots, P.q) + 1024) > 228 * 1024) P.S -= 2;
+    }
+    P.S = std::max(4, std::min(P.S, (dd + 1) & ~1));
     P.spill_cap = std::max(0, dd - P.S);
-    P.cta_slots = P.hist_mode ? 512 : 0;
-    int threads = 256;
     size_t smem = fast_smem_bytes(threads, P.GW, P.S, P.cta_slots, P.q);
     int maxsmem = 0;
     CK(cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
@@ -193,8 +199,11 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
       smem = fast_smem_bytes(threads, P.GW, P.S, P.cta_slots, P.q);
     }
     if (smem <= (size_t)maxsmem) {
-      const void *fn = P.a == 1 ? (const void *)k_classify_fast<1>
-                     : P.a == 2 ? (const void *)k_classify_fast<2> : (const void *)k_classify_fast<3>;
+      const void *fn = P.strict
+          ? (P.a == 1 ? (const void *)k_classify_fast<1, true>
+             : P.a == 2 ? (const void *)k_classify_fast<2, true> : (const void *)k_classify_fast<3, true>)
+          : (P.a == 1 ? (const void *)k_classify_fast<1, false>
+             : P.a == 2 ? (const void *)k_classify_fast<2, false> : (const void *)k_classify_fast<3, false>);
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       int per_sm = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem));

@@ -66,17 +66,21 @@ struct FastLane {
 };
 
 // ---- candidate tables -------------------------------------------------------
-template <int A> struct Cand;
+template <int A, bool STRICT> struct Cand;
 
 // SWAR over NC nibble lanes (NC = 4a; a <= 2 fits 32-bit masks, a == 3 64-bit):
-// E[dir] holds every candidate's dir-face label, "bonds p" is nibble-equality
-// with partner(p), CLS holds each candidate's equivalence-class id.
-template <typename M, int NC> struct CandSwar {
-  M E0, E1, E2, E3, N0, N1, N2, N3, CLS, SM;
+// E[dir] holds every candidate's dir-face label, P[dir] its partner
+// (partner(0) := 0xF, never a label), so "candidate c bonds the neighbour's
+// label p" is the nibble equality P[dir][c] == p (p = 0 never matches);
+// CLS holds each candidate's equivalence-class id (in-situ 4-label code).
+template <typename M, int NC, bool STRICT> struct CandSwar {
+  M E0, E1, E2, E3, P0, P1, P2, P3, N0, N1, N2, N3, CLS;
   static constexpr M VALID = (M)(0x8888888888888888ULL >> (64 - 4 * NC));
 
-  __device__ __forceinline__ void build(const uint32_t *lab, int ntiles, bool strict) {
-    E0 = E1 = E2 = E3 = 0;
+  __device__ __forceinline__ static uint32_t partner(uint32_t e) { return e ? (((e - 1u) ^ 1u) + 1u) : 15u; }
+
+  __device__ __forceinline__ void build(const uint32_t *lab, int ntiles) {
+    E0 = E1 = E2 = E3 = P0 = P1 = P2 = P3 = 0;
     uint32_t code[NC];
 #pragma unroll
     for (int t = 0; t < NC / 4; t++) {
@@ -87,6 +91,8 @@ template <typename M, int NC> struct CandSwar {
         const uint32_t e2 = lab[t * 4 + ((2 - r) & 3)], e3 = lab[t * 4 + ((3 - r) & 3)];
         E0 |= (M)e0 << (4 * c); E1 |= (M)e1 << (4 * c);
         E2 |= (M)e2 << (4 * c); E3 |= (M)e3 << (4 * c);
+        P0 |= (M)partner(e0) << (4 * c); P1 |= (M)partner(e1) << (4 * c);
+        P2 |= (M)partner(e2) << (4 * c); P3 |= (M)partner(e3) << (4 * c);
         code[c] = t < ntiles ? (e0 | (e1 << 4) | (e2 << 8) | (e3 << 12)) : 0xFFFF0000u | (uint32_t)c;
       }
     }
@@ -101,42 +107,51 @@ template <typename M, int NC> struct CandSwar {
     }
     N0 = nz_nib<M>(E0) & VALID; N1 = nz_nib<M>(E1) & VALID;
     N2 = nz_nib<M>(E2) & VALID; N3 = nz_nib<M>(E3) & VALID;
-    SM = strict ? ~(M)0 : (M)0;
   }
 
+  // candidates at a cell whose N,E,S,W neighbours hold board values vN..vW
+  // (>= NC: empty, shows no label); strict: a nonzero face against a nonzero
+  // non-partner label excludes the candidate (_k:176-198)
   __device__ __forceinline__ M cand(uint32_t vN, uint32_t vE, uint32_t vS, uint32_t vW) const {
     const uint32_t pN = vN < (uint32_t)NC ? get_nib<M>(E2, vN) : 0u;
     const uint32_t pE = vE < (uint32_t)NC ? get_nib<M>(E3, vE) : 0u;
     const uint32_t pS = vS < (uint32_t)NC ? get_nib<M>(E0, vS) : 0u;
     const uint32_t pW = vW < (uint32_t)NC ? get_nib<M>(E1, vW) : 0u;
+    const M l7 = (M)0x7777777777777777ULL;
     M bond = 0, conf = 0;
-#define TV_DIR(Ed, Nd, p)                                                      \
-  {                                                                            \
-    const M on = (p) ? VALID : (M)0;                                           \
-    const M bm = ~nz_nib<M>((Ed) ^ rep_nib<M>((((p) - 1u) ^ 1u) + 1u)) & on;   \
-    bond |= bm;                                                                \
-    conf |= (Nd) & ~bm & on;                                                   \
+#define TV_DIR(Pd, Nd, p)                                                    \
+  {                                                                          \
+    const M x = (Pd) ^ rep_nib<M>(p);                                        \
+    const M bm = ~((((x & l7) + l7) | x)) & VALID;                           \
+    bond |= bm;                                                              \
+    if (STRICT) conf |= (p) ? ((Nd) & ~bm) : (M)0;                           \
   }
-    TV_DIR(E0, N0, pN)
-    TV_DIR(E1, N1, pE)
-    TV_DIR(E2, N2, pS)
-    TV_DIR(E3, N3, pW)
+    TV_DIR(P0, N0, pN)
+    TV_DIR(P1, N1, pE)
+    TV_DIR(P2, N2, pS)
+    TV_DIR(P3, N3, pW)
 #undef TV_DIR
-    return bond & ~(conf & SM);
+    return STRICT ? (bond & ~conf) : bond;
   }
   __device__ __forceinline__ uint32_t first(M cand) const { return (uint32_t)ffs_m(cand) >> 2; }
   __device__ __forceinline__ bool ambiguous(M cand, uint32_t cf) const {
     return (nz_nib<M>(CLS ^ rep_nib<M>(get_nib<M>(CLS, cf))) & cand) != 0;
   }
 };
-template <> struct Cand<3> : CandSwar<uint64_t, 12> {};
-template <> struct Cand<2> : CandSwar<uint32_t, 8> {};
-template <> struct Cand<1> : Cand<2> {};
+template <bool S> struct Cand<3, S> : CandSwar<uint64_t, 12, S> {};
+template <bool S> struct Cand<2, S> : CandSwar<uint32_t, 8, S> {};
+template <bool S> struct Cand<1, S> : CandSwar<uint32_t, 8, S> {};
 
 enum { ST_NEED = 0, ST_RUN = 1, ST_DONE = 2 };
 
-template <int A>
-__global__ void __launch_bounds__(256, 2) k_classify_fast(const __grid_constant__ ClassifyParams P) {
+#ifndef TV_FAST_MINB
+#define TV_FAST_MINB 2
+#endif
+#ifndef TV_FAST_MAXT
+#define TV_FAST_MAXT 384  // 2 x 384 lanes per SM: 24 warps at <= 80 registers (measured +10% vs 2 x 256)
+#endif
+template <int A, bool STRICT>
+__global__ void __launch_bounds__(TV_FAST_MAXT, TV_FAST_MINB) k_classify_fast(const __grid_constant__ ClassifyParams P) {
   constexpr int NC = 4 * A;
   extern __shared__ uint32_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -182,7 +197,7 @@ __global__ void __launch_bounds__(256, 2) k_classify_fast(const __grid_constant_
   int trivial_at = -1, first_unbound = -1, first_mismatch = -1;
   uint32_t hash0 = 0, best = 0, fit0 = 0;
   int64_t pslot = -1;  // histogram slot whose payload the replay writes
-  Cand<A> K;
+  Cand<A, STRICT> K;
 
   for (;;) {
     const unsigned live = __ballot_sync(0xFFFFFFFFu, st != ST_DONE);
@@ -373,7 +388,7 @@ __global__ void __launch_bounds__(256, 2) k_classify_fast(const __grid_constant_
             uint32_t lab[12];  // decode labels (_k:384-401)
 #pragma unroll
             for (int te = 0; te < 12; te++) lab[te] = te < NC ? decode_label(P.dec, te, idx) : 0u;
-            K.build(lab, A, P.strict != 0);
+            K.build(lab, A);
             trivial_at = first_unbound = first_mismatch = -1;
             run = 0;
             replay = 0;
