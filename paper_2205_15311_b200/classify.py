@@ -22,6 +22,7 @@ import json
 import math
 import os
 import struct
+import threading
 import time
 from dataclasses import dataclass, field
 
@@ -429,6 +430,34 @@ class DeviceHistogram:
                                             P(np.ascontiguousarray(hist.shape)), P(tal), stream))
 
 
+_tls = threading.local()
+
+
+def _cached_histogram(ks, hist_k, W, capacity) -> "DeviceHistogram":
+    """Per-thread reusable device histogram (allocation and its implicit device
+    synchronisation stay out of repeated enumerate_space calls); cleared on reuse."""
+    import torch
+    key = (torch.cuda.current_device() if torch.cuda.is_available() else -1, tuple(ks), int(hist_k), int(W),
+           int(capacity))
+    cache = getattr(_tls, "hists", None)
+    if cache is None:
+        cache = _tls.hists = {}
+    h = cache.get(key)
+    if h is None or h._h is None:
+        h = cache[key] = DeviceHistogram(ks, hist_k, W, capacity)
+    else:
+        h.clear()
+    return h
+
+
+def _drop_cached_histogram(h) -> None:
+    cache = getattr(_tls, "hists", {})
+    for k, v in list(cache.items()):
+        if v is h:
+            del cache[k]
+    h.close()
+
+
 def shape_words_for(d: int) -> int:
     """u64 words for the largest bounded crop, (d-2) x (d-2) bits."""
     return max(1, ((d - 2) * (d - 2) + 63) // 64)
@@ -466,7 +495,7 @@ def enumerate_space(space: SearchSpace, d: int = 19, k: int = 8, seed: int = 0, 
     W = shape_words_for(d)
     plan = chunks if chunks is not None else chunk_plan(start, count, batch_size)
     meta = _space_meta(space, d, seed, strict)
-    dev = DeviceHistogram(ks, hist_k, W, capacity)
+    dev = _cached_histogram(ks, hist_k, W, capacity)
     done = 0
     if resume:
         prev, extra = Histogram.load(resume)
@@ -487,8 +516,9 @@ def enumerate_space(space: SearchSpace, d: int = 19, k: int = 8, seed: int = 0, 
             if checkpoint and ((ci + 1) % checkpoint_every == 0 or ci + 1 == len(plan)):
                 dev.export(meta=meta).save(checkpoint, extra=dict(chunks_done=ci + 1, chunks_total=len(plan)))
         out = dev.export(meta=meta)
-    finally:
-        dev.close()
+    except BaseException:
+        _drop_cached_histogram(dev)
+        raise
     out.meta["runtime_s"] = time.time() - t0
     out.meta["start"] = int(start)
     out.meta["count"] = int(count)

@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(TV_FAST_MAXT, TV_FAST_MINB) k_classify_fast(co
         const int dl = (dir & 1u) ? 1 : PD;
         const int nl = ((dir + 1u) & 2u) ? lin + dl : lin - dl;
         Ln.st_write(sp + j, (uint32_t)nl);
-        Ln.set_nib(nl, 0xEu);
+        Ln.gw[(nl >> 3) * 32] &= ~(1u << ((nl & 7) * 4));  // F -> E: on the movelist
       }
     }
     sp += mm;
