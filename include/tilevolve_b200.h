@@ -10,6 +10,8 @@
  *   tv_classify_single     <- _k.classify_single       _k:471-484
  *   tv_assemble_single     <- _k.assemble_single       _k:455-468
  *   tv_oat_hash_bytes      <- _k.oat_hash_bytes        _k:79-85
+ *   tv_shape_labels        <- classify.rotation_invariant_hash (absent module,
+ *                             SPEC.md:270-278) + the D4 min-hash label
  *   tv_enumerate_range     <- classify.enumerate_space (absent module;
  *   tv_enumerate_indices      SPEC.md:297-306, per-batch classify_batch calls
  *                             merged into a Histogram)
@@ -92,6 +94,16 @@ int tv_assemble_single(const uint8_t *edges, int32_t a, int32_t d, uint64_t seed
 
 /* _k:79-85: data [h|d] */
 int tv_oat_hash_bytes(const uint8_t *data, int64_t n, uint32_t *out);
+
+/* Canonical labels of n packed cropped shapes (extra columns; the histogram
+ * key stays the plain shape hash).  Replaces the host-side rotation-invariant
+ * hash of the absent classify module (caller asm:216-235)
+ * and adds the D4 (8 rotations + reflections) minimum shape hash.
+ * shape [h|d] u64[n*W] (bit y*w+x, _k:280-292), w/h [h|d] u8[n];
+ * out_rot4 / out_d4 [h|d] u32[n], either may be NULL.  Rows whose w*h
+ * exceeds W*64 bits or is zero get 0. */
+int tv_shape_labels(const uint64_t *shape, const uint8_t *w, const uint8_t *h, int64_t n, int64_t W,
+                    uint32_t *out_rot4, uint32_t *out_d4, void *stream);
 
 /* ---- phenotype histogram (device-resident, one CUDA device per handle) */
 typedef struct tv_hist tv_hist;

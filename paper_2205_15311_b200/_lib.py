@@ -52,6 +52,7 @@ _SIGS = {
     "tv_classify_single": (_i32, [_p, _i32, _i32, _i32, _u64, _u64, _i32, _p, _i64, _p]),
     "tv_assemble_single": (_i32, [_p, _i32, _i32, _u64, _u64, _i32, _i32, _p, _p]),
     "tv_oat_hash_bytes": (_i32, [_p, _i64, _p]),
+    "tv_shape_labels": (_i32, [_p, _p, _p, _i64, _i64, _p, _p, _p]),
     "tv_hist_create": (_i32, [_i64, _i32, _i32, ctypes.POINTER(_p)]),
     "tv_hist_destroy": (_i32, [_p]),
     "tv_hist_clear": (_i32, [_p, _p]),

@@ -157,7 +157,7 @@ def assemble_once(t: TileSet, d: int = DEFAULT_GRID_DIM, seed: int = 0, genome_i
 
 
 def _classify_rotation_invariant(t, d, k, seed, genome_index, strict_contacts) -> Classification:
-    from .classify import crop, rotation_invariant_hash
+    from .classify import crop, shape_labels
 
     outcomes = []
     for run in range(k):
@@ -169,7 +169,10 @@ def _classify_rotation_invariant(t, d, k, seed, genome_index, strict_contacts) -
     if any(o.kind is OutcomeKind.UNBOUND for o in outcomes):
         return Classification(ClassKind.UNBOUND)
     shapes = [crop(o.grid) for o in outcomes]
-    labels = {rotation_invariant_hash(s) for s in shapes}
+    W = max(1, (max(s.width * s.height for s in shapes) + 63) // 64)
+    rot4, _ = shape_labels([s.width for s in shapes], [s.height for s in shapes],
+                           np.stack([s.packed_words(W) for s in shapes]))
+    labels = {int(v) for v in rot4}
     if len(labels) > 1:
         return Classification(ClassKind.STERIC_NONDET)
     return Classification(ClassKind.DETERMINISTIC, labels.pop(), shapes[0])

@@ -322,6 +322,35 @@ class Histogram:
             return SearchSpace(m["a"], m["b"], tuple(tuple(x) for x in m.get("fixed_mask", ())))
         return None
 
+    # -- canonical phenotype classes (extra columns; the key stays the plain hash)
+    def canonical_labels(self, stream=None) -> dict:
+        """Per-record canonical labels computed on the device (tv_shape_labels):
+        ``rot4`` = SPEC.md:270-278 rotation-invariant hash, ``d4`` = minimum
+        shape hash over the 8 rotations and reflections."""
+        rot4, d4 = shape_labels(self.w, self.h, self.shape, stream=stream)
+        return dict(rot4=rot4, d4=d4)
+
+    def canonical_classes(self, kind: str = "d4", stream=None) -> dict:
+        """Records folded by canonical label: per label the summed det / steric
+        counts, the lowest representatives and how many plain hashes map to it.
+        Sorted by label."""
+        if kind not in ("d4", "rot4"):
+            raise ValueError("kind must be 'd4' or 'rot4'")
+        lab = self.canonical_labels(stream)[kind]
+        u, inv = np.unique(lab, return_inverse=True)
+        U = u.shape[0]
+        det = np.zeros(U, np.uint64)
+        ste = np.zeros(U, np.uint64)
+        np.add.at(det, inv, self.det)
+        np.add.at(ste, inv, self.steric)
+        big = np.iinfo(np.uint64).max
+        rep_det = np.full(U, big, np.uint64)
+        rep_any = np.full(U, big, np.uint64)
+        np.minimum.at(rep_det, inv, self.rep_det)
+        np.minimum.at(rep_any, inv, self.rep_any)
+        return dict(label=u.astype(np.uint32), det=det, steric=ste, rep_det=rep_det, rep_any=rep_any,
+                    hashes=np.bincount(inv, minlength=U).astype(np.int64))
+
     # -- checkpoint: versioned binary layout
     #   magic 8B | version u32 | header_len u32 | header JSON (utf-8) | arrays in header["arrays"] order, raw LE
     def save(self, path: str, extra: dict | None = None) -> None:
@@ -354,6 +383,22 @@ class Histogram:
                 arr = np.frombuffer(f.read(cnt * np.dtype(dt).itemsize), dtype=dt).reshape(shp).copy()
                 setattr(out, name, arr)
         return out, header["extra"]
+
+
+def shape_labels(w, h, shape, stream=None) -> tuple[np.ndarray, np.ndarray]:
+    """(rot4, d4) labels of packed cropped shapes on the device (tv_shape_labels).
+    ``shape`` is u64[n, W] (bit y*w+x, _k:280-292), ``w``/``h`` u8[n]."""
+    w = np.ascontiguousarray(w, np.uint8)
+    h = np.ascontiguousarray(h, np.uint8)
+    sh = np.ascontiguousarray(shape, np.uint64)
+    n = w.shape[0]
+    if sh.ndim != 2 or sh.shape[0] != n or h.shape[0] != n:
+        raise ValueError("shape must be [n, W] with n = len(w) = len(h)")
+    rot4 = np.zeros(n, np.uint32)
+    d4 = np.zeros(n, np.uint32)
+    P = _lib.ptr
+    _lib.check(_lib.lib().tv_shape_labels(P(sh), P(w), P(h), n, max(1, sh.shape[1]), P(rot4), P(d4), stream))
+    return rot4, d4
 
 
 class DeviceHistogram:

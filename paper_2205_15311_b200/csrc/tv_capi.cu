@@ -15,6 +15,7 @@
 #include "tv_fast.cuh"
 #include "tv_ga.cuh"
 #include "tv_kernels.cuh"
+#include "tv_shape.cuh"
 
 using namespace tvb;
 
@@ -414,6 +415,40 @@ int tv_oat_hash_bytes(const uint8_t *data, int64_t n, uint32_t *out) {
     CK(cudaMemcpyAsync(out, dout, 4, cudaMemcpyDeviceToHost, st));
   }
   CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+// ---------------------------------------------------------------- canonical shape labels
+int tv_shape_labels(const uint64_t *shape, const uint8_t *w, const uint8_t *h, int64_t n, int64_t W,
+                    uint32_t *out_rot4, uint32_t *out_d4, void *stream) {
+  if (n < 0) return fail(TV_ERR_ARG, "negative n");
+  if (W < 1) return fail(TV_ERR_ARG, "W must be >= 1");
+  if (!out_rot4 && !out_d4) return 0;
+  int dev;
+  if (int rc = current_device(&dev)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  bool any_host = false;
+  {
+    Scratch S(st);
+    uint64_t *d_shape; uint8_t *d_w, *d_h; uint32_t *d_r = nullptr, *d_d = nullptr;
+    bool h0, h1, h2, h3 = false, h4 = false;
+    if (int rc = stage_in(shape, (size_t)n * W, true, S, &d_shape, h0)) return rc;
+    if (int rc = stage_in(w, (size_t)n, true, S, &d_w, h1)) return rc;
+    if (int rc = stage_in(h, (size_t)n, true, S, &d_h, h2)) return rc;
+    if (out_rot4) if (int rc = stage_in(out_rot4, (size_t)n, false, S, &d_r, h3)) return rc;
+    if (out_d4) if (int rc = stage_in(out_d4, (size_t)n, false, S, &d_d, h4)) return rc;
+    any_host = h0 || h1 || h2 || h3 || h4;
+    if (n > 0) {
+      const int threads = 256;
+      const int64_t blocks = (n * 8 + threads - 1) / threads;
+      k_shape_labels<<<(unsigned)blocks, threads, 0, st>>>(reinterpret_cast<const unsigned long long *>(d_shape),
+                                                           d_w, d_h, n, W, d_r, d_d);
+      CK(cudaGetLastError());
+    }
+    if (h3) CK(cudaMemcpyAsync(out_rot4, d_r, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+    if (h4) CK(cudaMemcpyAsync(out_d4, d_d, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+  }
+  if (any_host) CK(cudaStreamSynchronize(st));
   return 0;
 }
 
