@@ -717,7 +717,7 @@ int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **
   e = e ? e : cudaMalloc(&P.pop0, n * 8);
   e = e ? e : cudaMalloc(&P.pop1, n * 8);
   e = e ? e : cudaMalloc(&P.cdf, n * 4);
-  e = e ? e : cudaMalloc(&P.guide, n * 4);
+  e = e ? e : cudaMalloc(&P.guide, (size_t)TV_GA_BUCKETS * n * 8);
   e = e ? e : cudaMalloc(&P.fstage, n * 4);
   e = e ? e : cudaMalloc(&P.tot, (size_t)h->nblocks * 8);
   e = e ? e : cudaMalloc(&P.done, 8);
@@ -783,6 +783,9 @@ int tv_ga_run(tv_ga *h, uint64_t seed, int64_t g0, int64_t n_gens, uint32_t targ
     CK(cudaMemsetAsync(d_count, 0, n_gens * 4, st));
     CK(cudaMemsetAsync(d_sum, 0, n_gens * 8, st));
     P.best = d_best; P.count = d_count; P.sum = d_sum;
+    P.prof = nullptr;
+    const bool prof = getenv("TV_GA_PROF") != nullptr;  // phase timing of CTA 0 (development aid)
+    if (prof) { CK(S.get(&P.prof, 3)); CK(cudaMemsetAsync(P.prof, 0, 24, st)); }
     void *args[] = {&P};
     CK(cudaLaunchCooperativeKernel((const void *)k_ga_run, dim3(h->nblocks), dim3(1024), args, h->smem, st));
     g_launch[0] = 3; g_launch[1] = h->nblocks; g_launch[2] = 1024; g_launch[3] = (int64_t)h->smem; g_launch[4] = 1;
@@ -791,6 +794,14 @@ int tv_ga_run(tv_ga *h, uint64_t seed, int64_t g0, int64_t n_gens, uint32_t targ
     if (best) CK(cudaMemcpyAsync(best, d_best, n_gens * 4, cudaMemcpyDefault, st));
     if (count) CK(cudaMemcpyAsync(count, d_count, n_gens * 4, cudaMemcpyDefault, st));
     if (sum) CK(cudaMemcpyAsync(sum, d_sum, n_gens * 8, cudaMemcpyDefault, st));
+    if (prof) {
+      unsigned long long ph[3];
+      CK(cudaMemcpyAsync(ph, P.prof, 24, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      const double g = (double)std::max<int64_t>(1, done);
+      fprintf(stderr, "tv_ga_run phases (CTA 0, us/gen): A+barrier %.2f  B+barrier %.2f  C %.2f\n",
+              ph[0] / g / 1e3, ph[1] / g / 1e3, ph[2] / g / 1e3);
+    }
   }
   CK(cudaStreamSynchronize(st));
   h->cur ^= fb;

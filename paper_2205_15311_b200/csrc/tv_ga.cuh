@@ -6,8 +6,9 @@
 //   -- grid barrier --
 //   B. chunk offsets -> global inclusive CDF (u32) and a guide table for
 //      indexed search (Chen & Asau): the r-range [0, total) is cut into
-//      B = min(n, total) monotone buckets b(r) = (r * M) >> 32 and guide[b] =
-//      the individual owning the first r of bucket b; individual j writes the
+//      B = min(2n, total) monotone buckets b(r) = (r * M) >> 32 and guide[b] =
+//      (cdf[j], j) of the individual j owning the first r of bucket b (so most
+//      lookups need no CDF load); individual j writes the
 //      buckets whose first r lies in its own range [cdf[j-1], cdf[j]), so the
 //      table is built in the same pass;
 //   -- grid barrier --
@@ -27,6 +28,13 @@
 
 #include "tv_device.cuh"
 
+#ifndef TV_GA_ILP
+#define TV_GA_ILP 2  // children per thread in flight in phase C (4 and 8 measured slower)
+#endif
+#ifndef TV_GA_BUCKETS
+#define TV_GA_BUCKETS 1  // guide buckets per individual
+#endif
+
 namespace tvb {
 
 struct GaParams {
@@ -45,14 +53,21 @@ struct GaParams {
   const uint32_t *f_ext;
   uint32_t *cdf;         // n
   uint32_t *fstage;      // n: fitness staged in index order (own chunk per CTA)
-  uint32_t *guide;       // n (first B entries used in a generation)
+  unsigned long long *guide;  // 2n: (cdf[j] << 32) | j per bucket (first B entries used in a generation)
   unsigned long long *tot;  // per CTA chunk totals
   uint32_t *best;        // n_gens
   unsigned long long *sum;  // n_gens
   uint32_t *count;       // n_gens
   unsigned long long *done;  // generations evaluated (written by CTA 0)
   int32_t *final_buf;    // which pop buffer holds the final population
+  unsigned long long *prof;  // optional (TV_GA_PROF): CTA 0 ns spent in phases A, B, C
 };
+
+__device__ __forceinline__ unsigned long long ga_clock() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ uint64_t ga_draw(uint64_t &s) {
   s += kGold;
@@ -106,18 +121,20 @@ __device__ __forceinline__ ChildDraws ga_draws(const GaParams &P, uint64_t gkey,
   return D;
 }
 
-// roulette: first j with cdf[j] > r, from the guide entry of r's bucket
+// roulette: first j with cdf[j] > r, from the guide entry of r's bucket; the
+// entry carries cdf[j] so a bucket whose owner covers r costs one load
 __device__ __forceinline__ uint32_t ga_pick(const GaParams &P, uint32_t r, uint32_t total, uint64_t mul) {
   if (total == 0) return r;
-  uint32_t j = P.guide[(uint32_t)(((uint64_t)r * mul) >> 32)];  // mul <= 2^32: no overflow
-  while (P.cdf[j] <= r) j++;
+  const unsigned long long e = P.guide[(uint32_t)(((uint64_t)r * mul) >> 32)];  // mul <= 2^32: no overflow
+  uint32_t j = (uint32_t)e, c = (uint32_t)(e >> 32);
+  while (c <= r) c = P.cdf[++j];
   return j;
 }
 
 __global__ void __launch_bounds__(1024, 1) k_ga_run(const __grid_constant__ GaParams P) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
-  __shared__ uint32_t warp_sum[32];
+  __shared__ uint32_t warp_sum[32];  // blockDim.x == 1024
   __shared__ uint32_t s_best, s_cnt;
   __shared__ unsigned long long s_off, s_total;
   __shared__ int s_stop;
@@ -125,8 +142,11 @@ __global__ void __launch_bounds__(1024, 1) k_ga_run(const __grid_constant__ GaPa
   const int64_t c0 = (int64_t)blockIdx.x * P.chunk;
   const int64_t c1 = min(P.n, c0 + P.chunk);
   const int64_t len = max((int64_t)0, c1 - c0);
-  const int64_t per = (len + nt - 1) / nt;     // contiguous items per thread
-  const int64_t i0 = c0 + tid * per, i1 = min(c1, i0 + per);
+  // phases A/B: warp w owns the contiguous segment [c0 + w*seg, c0 + (w+1)*seg)
+  // walked in rows of 32 consecutive individuals (coalesced loads and stores)
+  const int64_t seg = ((len + nt - 1) / nt) * 32;  // (rows per warp) x 32
+  const int64_t s0 = c0 + (int64_t)wid * seg;
+  const int rows = (int)(seg >> 5);
   int cur = 0;
   int64_t t = 0;
   // fitness of the initial population, staged in index order
@@ -138,46 +158,44 @@ __global__ void __launch_bounds__(1024, 1) k_ga_run(const __grid_constant__ GaPa
     const unsigned long long *pop = cur ? P.pop1 : P.pop0;
     unsigned long long *nxt = cur ? P.pop0 : P.pop1;
     if (tid == 0) { s_best = 0; s_cnt = 0; }
-    // ---- A: per-thread sums over a contiguous run of staged fitness, block scan, stats
+    const bool prof = P.prof && blockIdx.x == 0 && tid == 0;
+    unsigned long long tp0 = prof ? ga_clock() : 0ull, tp1 = 0ull;
+    // ---- A: warp sums over its segment, block scan of warp totals, stats
     uint32_t acc = 0, best = 0, cnt = 0;
-    for (int64_t i = i0; i < i1; i++) {
-      const uint32_t f = P.fstage[i];
+    for (int k = 0; k < rows; k++) {
+      const int64_t i = s0 + k * 32 + lane;
+      const uint32_t f = i < c1 ? P.fstage[i] : 0u;
       acc += f;
       best = max(best, f);
       cnt += f >= P.target;
     }
-    uint32_t x = acc;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
-      if (lane >= o) x += y;
+    for (int o = 16; o > 0; o >>= 1) {
+      acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+      best = max(best, __shfl_xor_sync(0xFFFFFFFFu, best, o));
+      cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
     }
-    if (lane == 31) warp_sum[wid] = x;
+    if (lane == 0) { warp_sum[wid] = acc; atomicMax(&s_best, best); atomicAdd(&s_cnt, cnt); }
     __syncthreads();
     if (wid == 0) {
-      uint32_t w = lane < (nt >> 5) ? warp_sum[lane] : 0u;
+      const uint32_t v = lane < (nt >> 5) ? warp_sum[lane] : 0u;
+      uint32_t w = v;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, w, o);
         if (lane >= o) w += y;
       }
-      warp_sum[lane] = w;
+      warp_sum[lane] = w - v;  // exclusive warp offsets
+      if (lane == 31) {
+        P.tot[blockIdx.x] = w;
+        atomicMax(&P.best[t], s_best);
+        atomicAdd(&P.count[t], s_cnt);
+      }
     }
     __syncthreads();
-    const uint32_t excl = x - acc + (wid ? warp_sum[wid - 1] : 0u);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      best = max(best, __shfl_xor_sync(0xFFFFFFFFu, best, o));
-      cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
-    }
-    if (lane == 0) { atomicMax(&s_best, best); atomicAdd(&s_cnt, cnt); }
-    __syncthreads();
-    if (tid == 0) {
-      P.tot[blockIdx.x] = warp_sum[(nt >> 5) - 1];
-      atomicMax(&P.best[t], s_best);
-      atomicAdd(&P.count[t], s_cnt);
-    }
+    const uint32_t excl = warp_sum[wid];
     grid.sync();
+    if (prof) { tp1 = ga_clock(); P.prof[0] += tp1 - tp0; tp0 = tp1; }
     // ---- B: chunk offsets -> global CDF + guide table; stop decision
     if (wid == 0) {
       unsigned long long o = 0, tt = 0;
@@ -200,53 +218,77 @@ __global__ void __launch_bounds__(1024, 1) k_ga_run(const __grid_constant__ GaPa
     }
     __syncthreads();
     const uint32_t total = (uint32_t)s_total;
-    // bucket function b(r) = (r * mul) >> 32, monotone, B = min(n, total) buckets
-    const uint64_t nb = min((uint64_t)P.n, (uint64_t)total);
+    // bucket function b(r) = (r * mul) >> 32, monotone, B = min(2n, total) buckets
+    // (r < total < 2^32 and mul <= 2^32, so r * mul fits 64 bits)
+    const uint64_t nb = min((uint64_t)TV_GA_BUCKETS * (uint64_t)P.n, (uint64_t)total);
     const uint64_t mul = total ? (nb << 32) / total : 0ull;
     if (blockIdx.x == 0 && tid == 0) P.sum[t] = s_total;
     if (s_stop) { t++; break; }
     {
-      uint32_t prev = (uint32_t)s_off + excl, run = prev;
-      for (int64_t i = i0; i < i1; i++) {
-        run += P.fstage[i];
-        P.cdf[i] = run;
-        if (run != prev) {  // own r in [prev, run): buckets whose first r falls in it
-          const int64_t b0 = prev ? (int64_t)(((uint64_t)(prev - 1) * mul) >> 32) + 1 : 0;
-          const int64_t b1 = (int64_t)(((uint64_t)(run - 1) * mul) >> 32);
-          for (int64_t b = b0; b <= b1; b++) P.guide[b] = (uint32_t)i;
+      uint32_t base = (uint32_t)s_off + excl;  // inclusive CDF before this warp's current row
+      for (int k = 0; k < rows; k++) {
+        const int64_t i = s0 + k * 32 + lane;
+        const uint32_t f = i < c1 ? P.fstage[i] : 0u;
+        uint32_t x = f;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+          if (lane >= o) x += y;
         }
-        prev = run;
+        const uint32_t run = base + x, prev = run - f;
+        if (i < c1) {
+          P.cdf[i] = run;
+          if (f) {  // own r in [prev, run): buckets whose first r falls in it
+            const int64_t b0 = prev ? (int64_t)(((uint64_t)(prev - 1) * mul) >> 32) + 1 : 0;
+            const int64_t b1 = (int64_t)(((uint64_t)(run - 1) * mul) >> 32);
+            const unsigned long long e = ((unsigned long long)run << 32) | (uint32_t)i;
+            for (int64_t b = b0; b <= b1; b++) P.guide[b] = e;
+          }
+        }
+        base = __shfl_sync(0xFFFFFFFFu, run, 31);
       }
     }
     grid.sync();
+    if (prof) { tp1 = ga_clock(); P.prof[1] += tp1 - tp0; tp0 = tp1; }
     const uint64_t gkey = mix64(P.seed ^ (kGold * ((uint64_t)g + 1)));  // stream_state prefix (_k:45-48)
-    // ---- C: children, two at a time (draws first, then the dependent loads);
+    // ---- C: children, TV_GA_ILP at a time (draws first, then the dependent loads);
     //      the next generation's fitness is staged as the children are made
-    for (int64_t i = c0 + tid; i < c1; i += 2 * nt) {
-      const int64_t i2 = i + nt;
-      const bool two = i2 < c1;
-      const ChildDraws D1 = ga_draws(P, gkey, i, total);
-      const ChildDraws D2 = two ? ga_draws(P, gkey, i2, total) : D1;
-      const uint32_t a1 = ga_pick(P, D1.ra, total, mul), a2 = ga_pick(P, D2.ra, total, mul);
-      uint64_t c1v = pop[a1], c2v = pop[a2];
-      if (P.mode != 0) {
-        const uint32_t b1 = ga_pick(P, D1.rb, total, mul), b2 = ga_pick(P, D2.rb, total, mul);
-        const uint64_t p1 = pop[b1], p2 = pop[b2];
-        c1v = (c1v & D1.top) | (p1 & ~D1.top);
-        c2v = (c2v & D2.top) | (p2 & ~D2.top);
+    constexpr int NI = TV_GA_ILP;
+    const uint64_t full = P.L == 64 ? ~0ULL : ((1ULL << P.L) - 1);
+    for (int64_t i = c0 + tid; i < c1; i += NI * nt) {
+      ChildDraws D[NI];
+      uint32_t pa[NI], pb[NI];
+#pragma unroll
+      for (int u = 0; u < NI; u++) {
+        const int64_t iu = i + u * nt;
+        D[u] = iu < c1 ? ga_draws(P, gkey, iu, total) : D[0];
       }
-      const uint64_t full = P.L == 64 ? ~0ULL : ((1ULL << P.L) - 1);
-      c1v = (c1v ^ D1.flips) & full;
-      nxt[i] = c1v;
-      if (P.fitness == 0) P.fstage[i] = (uint32_t)__popcll(c1v);
-      if (two) {
-        c2v = (c2v ^ D2.flips) & full;
-        nxt[i2] = c2v;
-        if (P.fitness == 0) P.fstage[i2] = (uint32_t)__popcll(c2v);
+#pragma unroll
+      for (int u = 0; u < NI; u++) pa[u] = ga_pick(P, D[u].ra, total, mul);
+      if (P.mode != 0) {
+#pragma unroll
+        for (int u = 0; u < NI; u++) pb[u] = ga_pick(P, D[u].rb, total, mul);
+      }
+      uint64_t cv[NI];
+#pragma unroll
+      for (int u = 0; u < NI; u++) cv[u] = pop[pa[u]];
+      if (P.mode != 0) {
+#pragma unroll
+        for (int u = 0; u < NI; u++) cv[u] = (cv[u] & D[u].top) | (pop[pb[u]] & ~D[u].top);
+      }
+#pragma unroll
+      for (int u = 0; u < NI; u++) {
+        const int64_t iu = i + u * nt;
+        if (iu < c1) {
+          const uint64_t c = (cv[u] ^ D[u].flips) & full;
+          nxt[iu] = c;
+          if (P.fitness == 0) P.fstage[iu] = (uint32_t)__popcll(c);
+        }
       }
     }
     cur ^= 1;
     __syncthreads();  // this CTA's staged fitness is read in index order by phase A
+    if (prof) P.prof[2] += ga_clock() - tp0;
   }
   if (blockIdx.x == 0 && tid == 0) {
     *P.done = (unsigned long long)t;
