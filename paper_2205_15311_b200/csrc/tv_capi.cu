@@ -215,6 +215,26 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
       const int64_t warps = blocks * (threads / 32);
       CK(S.get(&P.spill, (size_t)std::max(1, P.spill_cap) * 32 * warps));
       CK(S.get(&P.run_hash, (size_t)P.kmax * 32 * warps));
+      // early unbound cut-off: per-genome trivial-freedom bits from a full-SIMT pre-pass.
+      // Default on for a <= 2 (full S_{2,8}: 39.4 -> 38.9 ms incl. the 1.1 ms pre-pass);
+      // off for a = 3, where the 12-candidate proof costs more than it saves (S32
+      // 2^24 block: 42.7 -> 45.5 ms).  TV_EARLY_UNBOUND=0/1 forces it off/on.
+      const char *eu = getenv("TV_EARLY_UNBOUND");
+      P.tf_flags = nullptr;
+      if (eu ? atoi(eu) != 0 : P.a <= 2) {
+        uint32_t *flags;
+        const int64_t nw = (P.n + 31) / 32;
+        CK(S.get(&flags, (size_t)nw));
+        const void *ff = P.strict
+            ? (P.a == 1 ? (const void *)k_trivial_flags<1, true>
+               : P.a == 2 ? (const void *)k_trivial_flags<2, true> : (const void *)k_trivial_flags<3, true>)
+            : (P.a == 1 ? (const void *)k_trivial_flags<1, false>
+               : P.a == 2 ? (const void *)k_trivial_flags<2, false> : (const void *)k_trivial_flags<3, false>);
+        const int64_t fb = std::min<int64_t>((nw * 32 + 255) / 256, (int64_t)nsm * 8);
+        void *fargs[] = {&P, &flags};
+        CK(cudaLaunchKernel(ff, dim3((unsigned)fb), dim3(256), fargs, 0, st));
+        P.tf_flags = flags;
+      }
       void *args[] = {&P};
       CK(cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(threads), args, smem, st));
       g_launch[0] = 1; g_launch[1] = blocks; g_launch[2] = threads; g_launch[3] = (int64_t)smem; g_launch[4] = 1;

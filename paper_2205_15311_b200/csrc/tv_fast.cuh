@@ -79,9 +79,9 @@ template <typename M, int NC, bool STRICT> struct CandSwar {
 
   __device__ __forceinline__ static uint32_t partner(uint32_t e) { return e ? (((e - 1u) ^ 1u) + 1u) : 15u; }
 
-  __device__ __forceinline__ void build(const uint32_t *lab, int ntiles) {
+  // face labels and partners of every candidate (E, P); build() adds the rest
+  __device__ __forceinline__ void build_faces(const uint32_t *lab) {
     E0 = E1 = E2 = E3 = P0 = P1 = P2 = P3 = 0;
-    uint32_t code[NC];
 #pragma unroll
     for (int t = 0; t < NC / 4; t++) {
 #pragma unroll
@@ -93,7 +93,21 @@ template <typename M, int NC, bool STRICT> struct CandSwar {
         E2 |= (M)e2 << (4 * c); E3 |= (M)e3 << (4 * c);
         P0 |= (M)partner(e0) << (4 * c); P1 |= (M)partner(e1) << (4 * c);
         P2 |= (M)partner(e2) << (4 * c); P3 |= (M)partner(e3) << (4 * c);
-        code[c] = t < ntiles ? (e0 | (e1 << 4) | (e2 << 8) | (e3 << 12)) : 0xFFFF0000u | (uint32_t)c;
+      }
+    }
+  }
+
+  __device__ __forceinline__ void build(const uint32_t *lab, int ntiles) {
+    build_faces(lab);
+    uint32_t code[NC];
+#pragma unroll
+    for (int t = 0; t < NC / 4; t++) {
+#pragma unroll
+      for (int r = 0; r < 4; r++) {
+        const int c = t * 4 + r;
+        code[c] = t < ntiles ? (get_nib<M>(E0, c) | (get_nib<M>(E1, c) << 4) | (get_nib<M>(E2, c) << 8) |
+                                (get_nib<M>(E3, c) << 12))
+                             : 0xFFFF0000u | (uint32_t)c;
       }
     }
     CLS = 0;
@@ -136,6 +150,76 @@ template <typename M, int NC, bool STRICT> struct CandSwar {
   __device__ __forceinline__ uint32_t first(M cand) const { return (uint32_t)ffs_m(cand) >> 2; }
   __device__ __forceinline__ bool ambiguous(M cand, uint32_t cf) const {
     return (nz_nib<M>(CLS ^ rep_nib<M>(get_nib<M>(CLS, cf))) & cand) != 0;
+  }
+
+  // nibble c of X equals v -> bit 4c+3
+  __device__ __forceinline__ static M eqn(M X, uint32_t v) { return ~nz_nib<M>(X ^ rep_nib<M>(v)) & VALID; }
+
+  // Static proof that no run of this genome can end TRIVIAL (early unbound
+  // cut-off).  Over-approximates what a popped cell can
+  // see: R = candidates ever placeable (closure from the seed, candidate 0,
+  // under "bonds a label some candidate of R shows toward it from that side"),
+  // and a context = at most one label per side shown by R (empty sides are
+  // always compatible).  A TRIVIAL needs two hits with different in-situ codes
+  // in one context (_k:199-209): pair (c1, c2) can co-hit iff one side bonds
+  // both (same partner label), or two different sides bond one each while the
+  // other candidate tolerates that label (strict: its face there is 0 or
+  // bonds it, _k:176-198).  No such pair -> TRIVIAL is impossible.
+  __device__ __forceinline__ bool trivial_free() const {
+    const M E[4] = {E0, E1, E2, E3}, Pt[4] = {P0, P1, P2, P3};
+    M U[NC];  // U[c2]: candidates c that show c2's partner label on some side facing c2
+#pragma unroll
+    for (int c2 = 0; c2 < NC; c2++) {
+      U[c2] = 0;
+#pragma unroll
+      for (int k = 0; k < 4; k++) U[c2] |= eqn(E[(k + 2) & 3], get_nib<M>(Pt[k], c2));
+    }
+    M Rn = (M)8;  // candidate 0 (the seed) in nibble-flag form
+#pragma unroll 1
+    for (int it = 0; it < NC; it++) {
+      M R2 = Rn;
+#pragma unroll
+      for (int c2 = 0; c2 < NC; c2++) R2 |= (U[c2] & Rn) ? ((M)8 << (4 * c2)) : (M)0;
+      if (R2 == Rn) break;
+      Rn = R2;
+    }
+    // S[k]: labels a placeable candidate can show toward a cell from side k (bit per label)
+    uint32_t S[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int c = 0; c < NC; c++) {
+      const uint32_t in = (uint32_t)((Rn >> (4 * c + 3)) & 1u);
+#pragma unroll
+      for (int k = 0; k < 4; k++) S[k] |= in << get_nib<M>(E[(k + 2) & 3], c);
+    }
+    // per candidate, nibble-flag form (bit 4k+3 <-> side k): sides that can bond it, zero faces;
+    // packed partner labels (partner() is injective, so equal packs <=> equal codes, _k:199)
+    uint32_t bond[NC], z[NC], pc[NC];
+#pragma unroll
+    for (int c = 0; c < NC; c++) {
+      bond[c] = 0u; z[c] = 0u; pc[c] = 0u;
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const uint32_t pk = get_nib<M>(Pt[k], c);
+        bond[c] |= ((S[k] >> pk) & 1u) << (4 * k + 3);  // partner 15 (face 0) is never shown
+        pc[c] |= pk << (4 * k);
+      }
+      z[c] = ~nz_nib<uint32_t>((uint32_t)(((E0 >> (4 * c)) & 15u) | (((E1 >> (4 * c)) & 15u) << 4) |
+                                          (((E2 >> (4 * c)) & 15u) << 8) | (((E3 >> (4 * c)) & 15u) << 12))) &
+             0x8888u;
+    }
+    bool ok = true;
+#pragma unroll
+    for (int c1 = 0; c1 < NC; c1++) {
+#pragma unroll
+      for (int c2 = c1 + 1; c2 < NC; c2++) {
+        const uint32_t same = ~nz_nib<uint32_t>(pc[c1] ^ pc[c2]) & 0x8888u;  // same partner label per side
+        const uint32_t b1 = bond[c1] & (STRICT ? (same | z[c2]) : 0x8888u);
+        const uint32_t b2 = bond[c2] & (STRICT ? (same | z[c1]) : 0x8888u);
+        const bool pair = (bond[c1] & same) != 0u || (b1 && b2 && !(b1 == b2 && (b1 & (b1 - 1u)) == 0u));
+        ok = ok && !(pair && pc[c1] != pc[c2]);  // equal partner codes <=> equal in-situ codes
+      }
+    }
+    return ok;
   }
 };
 template <bool S> struct Cand<3, S> : CandSwar<uint64_t, 12, S> {};
@@ -197,6 +281,7 @@ __global__ void __launch_bounds__(TV_FAST_MAXT, TV_FAST_MINB) k_classify_fast(co
   int trivial_at = -1, first_unbound = -1, first_mismatch = -1;
   uint32_t hash0 = 0, best = 0, fit0 = 0;
   int64_t pslot = -1;  // histogram slot whose payload the replay writes
+  bool tfree = false;  // no run of this genome can go TRIVIAL (k_trivial_flags)
   Cand<A, STRICT> K;
 
   for (;;) {
@@ -273,8 +358,13 @@ __global__ void __launch_bounds__(TV_FAST_MAXT, TV_FAST_MINB) k_classify_fast(co
             if (run == 0) { hash0 = hs; fit0 = (uint32_t)n | ((uint32_t)ov << 16); }
             else if (first_mismatch < 0 && first_unbound != 0 && hs != hash0) first_mismatch = run;
           } else if (ended == RUN_UNBOUND) {
-            if (first_unbound < 0) first_unbound = run;
             rh[run * 32] = 0u;
+            if (first_unbound < 0) {
+              first_unbound = run;
+              // early unbound cut-off: every prefix k' > run is now UNBOUND unless a
+              // later run goes TRIVIAL, which the genome's flag proves impossible
+              if (tfree) done = true;
+            }
           } else {
             done = true;
             if (ended == RUN_TRIVIAL) trivial_at = run;
@@ -389,6 +479,7 @@ __global__ void __launch_bounds__(TV_FAST_MAXT, TV_FAST_MINB) k_classify_fast(co
 #pragma unroll
             for (int te = 0; te < 12; te++) lab[te] = te < NC ? decode_label(P.dec, te, idx) : 0u;
             K.build(lab, A);
+            tfree = P.tf_flags ? ((P.tf_flags[item >> 5] >> (item & 31)) & 1u) != 0u : false;
             trivial_at = first_unbound = first_mismatch = -1;
             run = 0;
             replay = 0;
@@ -487,6 +578,32 @@ __global__ void __launch_bounds__(TV_FAST_MAXT, TV_FAST_MINB) k_classify_fast(co
     }
     for (int s = threadIdx.x; s < P.q * 5; s += blockDim.x)
       if (c_tal[s]) atomicAdd(&P.hist.tallies[s], (unsigned long long)c_tal[s]);
+  }
+}
+
+// Per-item trivial-freedom bits for the early unbound cut-off: bit (i & 31)
+// of flags[i >> 5] for work item i.  Full-SIMT pre-pass (every lane runs the
+// same straight-line proof), so the divergent fold in k_classify_fast only
+// reads one bit.
+template <int A, bool STRICT>
+__global__ void __launch_bounds__(256) k_trivial_flags(const __grid_constant__ ClassifyParams P, uint32_t *flags) {
+  constexpr int NC = 4 * A;
+  const int64_t nw = (P.n + 31) >> 5;
+  for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~(int64_t)31; base < nw * 32;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t item = base + (threadIdx.x & 31);
+    bool f = false;
+    if (item < P.n) {
+      const uint64_t idx = item_index(P.indices, P.start, P.chunk, P.stride, item);
+      uint32_t lab[12];
+#pragma unroll
+      for (int te = 0; te < 12; te++) lab[te] = te < NC ? decode_label(P.dec, te, idx) : 0u;
+      Cand<A, STRICT> K;
+      K.build_faces(lab);  // tiles >= A have all-zero faces: they never bond, so never pair
+      f = K.trivial_free();
+    }
+    const uint32_t w = __ballot_sync(0xFFFFFFFFu, f);
+    if ((threadIdx.x & 31) == 0) flags[base >> 5] = w;
   }
 }
 

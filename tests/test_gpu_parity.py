@@ -157,3 +157,43 @@ def test_enumerate_generic_path_histogram(K):
     exp = G.histogram_from_outputs(c["expected"], c["idx"], c["ks"], c["hist_k"])
     for k in ("keys", "det", "steric", "rep_det", "rep_any", "tallies"):
         assert np.array_equal(getattr(h, k).astype(np.int64), exp[k].astype(np.int64)), k
+
+
+@pytest.fixture
+def early_unbound(monkeypatch):
+    """Force the early-unbound cut-off on/off (read per launch from TV_EARLY_UNBOUND)."""
+    def set_(on: bool):
+        monkeypatch.setenv("TV_EARLY_UNBOUND", "1" if on else "0")
+    return set_
+
+
+@pytest.mark.parametrize("on", [False, True])
+def test_early_unbound_cutoff_s28_full(K, early_unbound, on):
+    """The cut-off stops a genome at its first UNBOUND run only when no run can go
+    TRIVIAL; the full-S28 histogram must not change either way."""
+    from paper_2205_15311_b200.classify import enumerate_space
+    from paper_2205_15311_b200.genome import SearchSpace
+    early_unbound(on)
+    h = enumerate_space(SearchSpace(2, 8), d=19, ks=(1, 2, 4, 8), seed=0, batch_size=1 << 24)
+    _check_hist(h, "s28_full")
+
+
+@pytest.mark.parametrize("on", [False, True])
+def test_early_unbound_cutoff_per_genome(K, early_unbound, on):
+    """Per-genome rows (every column, every prefix k) with the cut-off forced on/off,
+    for a = 1, 2, 3 and non-strict contacts, against the pinned oracle."""
+    from oracle import oracle as O
+    early_unbound(on)
+    rng = np.random.default_rng(21)
+    cases = [(S28_ARGS, (1, 2, 4, 8), 8, True, 1 << 24), (S32_ARGS, (1, 3, 7), 7, True, 1 << 32),
+             (S32_ARGS, (2, 5), 5, False, 1 << 32),
+             ((1, 3, np.zeros(0, np.int64), np.zeros(0, np.uint8), np.arange(11, -1, -1, dtype=np.int64)),
+              (1, 8), 4, True, 1 << 12)]
+    for args, ks, hk, strict, space in cases:
+        idx = rng.integers(0, space, 1 << 17, dtype=np.uint64)
+        a = G.fresh_outputs(idx.shape[0], len(ks))
+        b = G.fresh_outputs(idx.shape[0], len(ks))
+        K.classify_batch(idx, *args, 19, np.array(ks), hk, np.uint64(5), strict, *[a[k] for k in G.OUT_KEYS])
+        O.classify_batch(idx, *args, 19, np.array(ks), hk, 5, strict, *[b[k] for k in G.OUT_KEYS])
+        for k in G.OUT_KEYS:
+            assert np.array_equal(a[k], b[k]), (args[0], ks, strict, k)
