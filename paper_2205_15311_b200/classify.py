@@ -228,7 +228,7 @@ class Histogram:
                 out.tallies[j, col] = int(np.count_nonzero(c == v))
         hc = cls_[:, ks.index(int(hist_k))]
         sel = np.nonzero((hc == 0) | (hc == 2))[0]
-        keys, first, inv = np.unique(np.asarray(out_hash)[sel], return_index=True, return_inverse=True)
+        keys, inv = np.unique(np.asarray(out_hash)[sel], return_inverse=True)
         U = keys.shape[0]
         isdet = hc[sel] == 0
         out.keys = keys.astype(np.uint32)
@@ -239,7 +239,10 @@ class Histogram:
         out.rep_any = np.full(U, big, np.uint64)
         np.minimum.at(out.rep_any, inv, idx[sel])
         np.minimum.at(out.rep_det, inv[isdet], idx[sel][isdet])
-        rows = sel[first]
+        # payload = the representative's row (lowest index per key), whatever the row order
+        order = np.lexsort((idx[sel], inv))
+        starts = np.r_[0, np.flatnonzero(np.diff(inv[order])) + 1]
+        rows = sel[order[starts]]
         out.w = np.asarray(out_w)[rows].astype(np.uint8)
         out.h = np.asarray(out_h)[rows].astype(np.uint8)
         out.cells = np.asarray(out_cells)[rows].astype(np.uint16)
@@ -271,9 +274,11 @@ class Histogram:
             r = np.full(U, np.iinfo(np.uint64).max, np.uint64)
             np.minimum.at(r, inv, np.concatenate([getattr(p, n) for p in parts]))
             setattr(out, n, r)
-        first_pos = np.full(U, -1, np.int64)
-        order = np.arange(keys.shape[0])[::-1]
-        first_pos[inv[order]] = order
+        # payload of each key = the one travelling with its lowest rep_any (ties: first part)
+        ra = np.concatenate([p.rep_any for p in parts])
+        order = np.lexsort((np.arange(keys.shape[0]), ra, inv))
+        starts = np.r_[0, np.flatnonzero(np.diff(inv[order])) + 1] if keys.shape[0] else np.zeros(0, np.int64)
+        first_pos = order[starts]
         for n in ("w", "h", "cells"):
             setattr(out, n, np.concatenate([getattr(p, n) for p in parts])[first_pos])
         out.shape = np.concatenate([p.shape for p in parts])[first_pos].reshape(U, first.W)

@@ -298,7 +298,66 @@ __global__ void __launch_bounds__(256) k_int_peak(int64_t iters, uint32_t seed, 
 struct tv_hist {
   HistDev H;
   int device;
+  bool has_params = false;  // enumeration parameters of the genomes counted since the last clear
+  Common params;            // (needed to re-classify representatives for their payloads)
 };
+
+namespace {
+// same space / k / seed / contact rule: histogram contents stay consistent
+bool same_enumeration(const ClassifyParams &a, const ClassifyParams &b) {
+  if (memcmp(&a.dec, &b.dec, sizeof a.dec) != 0) return false;
+  if (a.a != b.a || a.d != b.d || a.strict != b.strict || a.q != b.q || a.kmax != b.kmax || a.hist_k != b.hist_k ||
+      a.seed != b.seed)
+    return false;
+  for (int i = 0; i < a.q; i++)
+    if (a.ks[i] != b.ks[i]) return false;
+  return true;
+}
+
+// Fill the payload of every slot whose payload is not its representative's
+// (tv_hist.cuh): re-classify those representatives (classify mode, one call).
+int fix_payloads(tv_hist *h, cudaStream_t st) {
+  const HistDev &H = h->H;
+  Scratch S(st);
+  unsigned int *cnt;
+  uint32_t *slots;
+  unsigned long long *idx;
+  unsigned int nkeys = 0;
+  CK(cudaMemcpyAsync(&nkeys, H.n_keys, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (nkeys == 0) return 0;
+  CK(S.get(&cnt, 2)); CK(S.get(&slots, nkeys)); CK(S.get(&idx, nkeys));
+  CK(cudaMemsetAsync(cnt, 0, 8, st));
+  k_hist_stale<<<256, 256, 0, st>>>(H, slots, idx, cnt);
+  CK(cudaGetLastError());
+  unsigned int ns = 0;
+  CK(cudaMemcpyAsync(&ns, cnt, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (ns == 0) return 0;
+  if (!h->has_params)
+    return fail(TV_ERR_ARG, "%u histogram records lack their representative's payload and no enumeration "
+                            "parameters are known (merge complete records or enumerate into this histogram)", ns);
+  Common C = h->params;
+  ClassifyParams &P = C.P;
+  P.hist_mode = 0; P.fit_mode = 0; P.indices = reinterpret_cast<const uint64_t *>(idx); P.n = ns;
+  P.start = 0; P.chunk = 0; P.stride = 0;
+  uint8_t *cls, *w, *hh; uint32_t *hash; uint16_t *cells; unsigned long long *shape;
+  CK(S.get(&cls, (size_t)ns * P.q)); CK(S.get(&hash, ns)); CK(S.get(&w, ns)); CK(S.get(&hh, ns));
+  CK(S.get(&cells, ns)); CK(S.get(&shape, (size_t)ns * H.W));
+  P.out_class = cls; P.out_hash = hash; P.out_w = w; P.out_h = hh; P.out_cells = cells; P.out_shape = shape;
+  P.W = H.W;
+  if (int rc = launch_classify(C, S, st)) return rc;
+  const int blocks = (int)std::min<int64_t>(256, ((int64_t)ns + 255) / 256);
+  k_hist_payload<<<blocks, 256, 0, st>>>(H, slots, idx, ns, hash, w, hh, cells, shape, cnt + 1);
+  CK(cudaGetLastError());
+  unsigned int err = 0;
+  CK(cudaMemcpyAsync(&err, cnt + 1, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (err) return fail(TV_ERR_ARG, "a representative did not reproduce its hash: the histogram mixes "
+                                   "enumeration parameters");
+  return 0;
+}
+}  // namespace
 
 extern "C" {
 
@@ -492,6 +551,7 @@ int tv_hist_create(int64_t capacity, int32_t q, int32_t W, tv_hist **out) {
   e = e ? e : cudaMalloc(&H.rep_det, cap * 8);
   e = e ? e : cudaMalloc(&H.rep_any, cap * 8);
   e = e ? e : cudaMalloc(&H.whc, cap * 4);
+  e = e ? e : cudaMalloc(&H.pay_idx, cap * 8);
   e = e ? e : cudaMalloc(&H.shape, cap * 8 * W);
   e = e ? e : cudaMalloc(&H.tallies, (size_t)q * 5 * 8);
   e = e ? e : cudaMalloc(&H.n_keys, 4);
@@ -510,13 +570,15 @@ int tv_hist_destroy(tv_hist *h) {
   if (!h) return 0;
   HistDev &H = h->H;
   cudaFree(H.keys); cudaFree(H.det); cudaFree(H.steric); cudaFree(H.rep_det); cudaFree(H.rep_any);
-  cudaFree(H.whc); cudaFree(H.shape); cudaFree(H.tallies); cudaFree(H.n_keys); cudaFree(H.overflow);
+  cudaFree(H.whc); cudaFree(H.pay_idx); cudaFree(H.shape); cudaFree(H.tallies); cudaFree(H.n_keys);
+  cudaFree(H.overflow);
   delete h;
   return 0;
 }
 
 int tv_hist_clear(tv_hist *h, void *stream) {
   if (!h) return fail(TV_ERR_ARG, "null histogram");
+  h->has_params = false;
   k_hist_reset<<<256, 256, 0, (cudaStream_t)stream>>>(h->H);
   CK(cudaGetLastError());
   return 0;
@@ -543,6 +605,7 @@ int tv_hist_export(tv_hist *h, int64_t max_records, uint32_t *keys, uint64_t *de
   int32_t ovf = 0;
   if (int rc = tv_hist_count(h, &n, &ovf, stream)) return rc;
   if (ovf) return fail(TV_ERR_HIST_FULL, "histogram overflowed its %lld slots", (long long)h->H.cap);
+  if (int rc = fix_payloads(h, st)) return rc;
   if (n > max_records) return fail(TV_ERR_ARG, "%lld records do not fit max_records=%lld", (long long)n, (long long)max_records);
   const HistDev &H = h->H;
   {
@@ -635,6 +698,10 @@ static int enumerate_common(const uint64_t *indices, uint64_t start, uint64_t ch
   if (int rc = fill_common(a, bpl, mask_pos, mask_val, m, free_pos, nfree, d, ks, q, hist_k, seed, strict, C)) return rc;
   if (q != h->H.q) return fail(TV_ERR_ARG, "histogram was created for q=%d, got %lld", h->H.q, (long long)q);
   if ((int64_t)h->H.W * 64 < (int64_t)(d - 2) * (d - 2)) return fail(TV_ERR_ARG, "histogram W too small for d=%d", d);
+  if (h->has_params && !same_enumeration(h->params.P, C.P))
+    return fail(TV_ERR_ARG, "histogram holds genomes enumerated with other parameters (space, ks, seed, d or "
+                            "contact rule); clear it first");
+  if (!h->has_params) { h->params = C; h->has_params = true; }
   cudaStream_t st = (cudaStream_t)stream;
   bool host = false;
   {

@@ -3,7 +3,12 @@
 // Open-addressed global table keyed by the 32-bit shape hash.  Per key:
 // det/steric genome counts, the lowest DET index and the lowest DET-or-STERIC
 // index ("representative = lowest enumeration index"), and the
-// payload (w, h, cells, cropped bitmap) which is a function of the hash.
+// payload (w, h, cells, cropped bitmap) of the representative rep_any: the
+// enumeration kernels only count; tv_hist_export fills the payload of every
+// slot whose pay_idx is not its rep_any by re-classifying that one genome, so
+// colliding shapes under one 32-bit hash resolve to the lowest index exactly
+// as the per-genome aggregation does (with ~5e5 keys in S32, distinct shapes
+// sharing a 32-bit hash are expected).
 // Global class tallies per prefix k (DET, TRIV, STERIC, UNB, ERROR).
 #pragma once
 #include <cstdint>
@@ -18,6 +23,7 @@ struct HistDev {
   unsigned long long *rep_det;   // cap; ~0 = none
   unsigned long long *rep_any;   // cap
   uint32_t *whc;                 // cap; w | h<<8 | cells<<16
+  unsigned long long *pay_idx;   // cap; genome whose payload whc/shape hold (~0 = none)
   unsigned long long *shape;     // cap * W
   unsigned long long *tallies;   // q * 5
   unsigned int *n_keys;          // claimed slots

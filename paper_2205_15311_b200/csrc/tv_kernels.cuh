@@ -48,34 +48,23 @@ __global__ void __launch_bounds__(128) k_classify_generic(const __grid_constant_
       if (!P.hist_mode) { P.out_hash[item] = 0; P.out_w[item] = 0; P.out_h[item] = 0; P.out_cells[item] = 0; }
       continue;
     }
-    unsigned long long *dst = nullptr;
-    int64_t W = 0, g = -1;
-    if (!P.hist_mode) {
-      dst = P.out_shape + item * P.W;
-      W = P.W;
-    } else {
+    if (P.hist_mode) {  // count only; the representative's payload is filled at export
       bool gnew = false;
-      g = hist_claim(P.hist, F.hash, gnew);
+      const int64_t g = hist_claim(P.hist, F.hash, gnew);
       if (g < 0) continue;
       const bool det = hc == CLS_DET;
       atomicAdd(det ? &P.hist.det[g] : &P.hist.steric[g], 1ULL);
       if (det) hist_min(&P.hist.rep_det[g], idx);
       hist_min(&P.hist.rep_any[g], idx);
-      if (!gnew) continue;
-      dst = P.hist.shape + g * P.hist.W;
-      W = P.hist.W;
+      continue;
     }
     // replay the attributed run (identical substream) to emit its bitmap
     GRun R = g_assemble(edges, P.a, P.d, P.strict, P.seed, idx, F.attr_run, V);
     int w, h, nc;
-    g_hash_region(V, P.d, R, w, h, nc, dst, W);
+    g_hash_region(V, P.d, R, w, h, nc, P.out_shape + item * P.W, P.W);
     g_cleanup(V, R);
-    if (!P.hist_mode) {
-      P.out_hash[item] = F.hash;
-      P.out_w[item] = (uint8_t)w; P.out_h[item] = (uint8_t)h; P.out_cells[item] = (uint16_t)nc;
-    } else {
-      P.hist.whc[g] = (uint32_t)w | ((uint32_t)h << 8) | ((uint32_t)nc << 16);
-    }
+    P.out_hash[item] = F.hash;
+    P.out_w[item] = (uint8_t)w; P.out_h[item] = (uint8_t)h; P.out_cells[item] = (uint16_t)nc;
   }
 }
 
@@ -121,7 +110,7 @@ __global__ void k_oat(const uint8_t *p, int64_t n, uint32_t *out) {
 __global__ void k_hist_reset(HistDev H) {
   for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < H.cap; s += (int64_t)gridDim.x * blockDim.x) {
     H.keys[s] = 0ULL; H.det[s] = 0ULL; H.steric[s] = 0ULL;
-    H.rep_det[s] = ~0ULL; H.rep_any[s] = ~0ULL; H.whc[s] = 0u;
+    H.rep_det[s] = ~0ULL; H.rep_any[s] = ~0ULL; H.whc[s] = 0u; H.pay_idx[s] = ~0ULL;
   }
   if (blockIdx.x == 0) {
     for (int i = threadIdx.x; i < H.q * 5; i += blockDim.x) H.tallies[i] = 0ULL;
@@ -137,6 +126,31 @@ __global__ void k_hist_compact(HistDev H, uint32_t *keys_out, uint32_t *slot_out
       keys_out[p] = (uint32_t)k;
       slot_out[p] = (uint32_t)s;
     }
+  }
+}
+
+// slots whose payload does not belong to their representative (rep_any)
+__global__ void k_hist_stale(HistDev H, uint32_t *slot_out, unsigned long long *idx_out, unsigned int *cnt) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < H.cap; s += (int64_t)gridDim.x * blockDim.x) {
+    if (H.keys[s] && H.pay_idx[s] != H.rep_any[s]) {
+      const unsigned int p = atomicAdd(cnt, 1u);
+      slot_out[p] = (uint32_t)s;
+      idx_out[p] = H.rep_any[s];
+    }
+  }
+}
+
+// payload rows of the re-classified representatives -> their slots; a hash
+// that does not reproduce the slot key flags an error
+__global__ void k_hist_payload(HistDev H, const uint32_t *slots, const unsigned long long *idx, int64_t n,
+                               const uint32_t *hash, const uint8_t *w, const uint8_t *h, const uint16_t *cells,
+                               const unsigned long long *shape, unsigned int *err) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = slots[i];
+    if (hash[i] != (uint32_t)H.keys[s]) { atomicOr(err, 1u); continue; }
+    H.whc[s] = (uint32_t)w[i] | ((uint32_t)h[i] << 8) | ((uint32_t)cells[i] << 16);
+    for (int j = 0; j < H.W; j++) H.shape[s * H.W + j] = shape[i * H.W + j];
+    H.pay_idx[s] = idx[i];
   }
 }
 
@@ -168,10 +182,14 @@ __global__ void k_hist_merge(HistDev H, int64_t n, HistRecords R, const long lon
     if (R.steric[i]) atomicAdd(&H.steric[g], R.steric[i]);
     if (R.rep_det[i] != ~0ULL) hist_min(&H.rep_det[g], R.rep_det[i]);
     if (R.rep_any[i] != ~0ULL) hist_min(&H.rep_any[g], R.rep_any[i]);
-    if (gnew) {
+    // an incoming record carries its representative's payload: keep the lowest one
+    // (keys are unique within one merge call, so no other thread touches slot g here)
+    if (R.rep_any[i] != ~0ULL && R.rep_any[i] < H.pay_idx[g]) {
       H.whc[g] = (uint32_t)R.w[i] | ((uint32_t)R.h[i] << 8) | ((uint32_t)R.cells[i] << 16);
       for (int j = 0; j < H.W; j++) H.shape[g * H.W + j] = R.shape[i * H.W + j];
+      H.pay_idx[g] = R.rep_any[i];
     }
+    (void)gnew;
   }
   if (tallies && blockIdx.x == 0)
     for (int i = threadIdx.x; i < H.q * 5; i += blockDim.x)

@@ -7,8 +7,10 @@ c mod R) because work varies strongly with the high index bits (the seed
 tile's labels).  The only exchange is at the end: the per-rank histograms are
 combined by ``allreduce_histogram`` -- an all-gather of the (tiny) key sets to
 build the same sorted key union on every rank, then dense all-reduces over
-that union: SUM for counts and class tallies, MIN for representatives, MAX
-for the payload (identical wherever present).  With the NCCL backend the
+that union: SUM for counts and class tallies, MIN for representatives, then
+MAX over the payloads where only the rank holding the representative (lowest
+rep_any) contributes, so colliding shapes under one hash resolve exactly as
+the per-genome aggregation does.  With the NCCL backend the
 tensors live in HBM and the collectives run over NVLink; the same code runs on
 gloo/CPU for the multi-process tests.
 """
@@ -65,12 +67,14 @@ def allreduce_histogram(h: Histogram, group=None) -> Histogram:
     mins[pos] = rep(h.rep_det)
     mins[U + pos] = rep(h.rep_any)
     W = h.W
-    maxs = torch.full((U, 1 + W), I64_MIN, dtype=torch.int64, device=dev)
-    whc = h.w.astype(np.int64) | (h.h.astype(np.int64) << 8) | (h.cells.astype(np.int64) << 16)
-    maxs[pos, 0] = torch.from_numpy(whc).to(dev)
-    maxs[pos, 1:] = torch.from_numpy(np.ascontiguousarray(h.shape).view(np.int64)).to(dev)
     dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
     dist.all_reduce(mins, op=dist.ReduceOp.MIN, group=group)
+    # payload = the representative's (lowest rep_any): only the rank holding it contributes
+    maxs = torch.full((U, 1 + W), I64_MIN, dtype=torch.int64, device=dev)
+    whc = h.w.astype(np.int64) | (h.h.astype(np.int64) << 8) | (h.cells.astype(np.int64) << 16)
+    own = rep(h.rep_any) == mins[U + pos]
+    maxs[pos[own], 0] = torch.from_numpy(whc).to(dev)[own]
+    maxs[pos[own], 1:] = torch.from_numpy(np.ascontiguousarray(h.shape).view(np.int64)).to(dev)[own]
     dist.all_reduce(maxs, op=dist.ReduceOp.MAX, group=group)
     s = sums.cpu().numpy()
     m = mins.cpu().numpy()

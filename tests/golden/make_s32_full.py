@@ -4,7 +4,9 @@ The reference (numba) needs ~1.4 h on 8 cores for the 2^32 genomes; the C
 restatement in oracle/ is pinned to the reference by tests/test_oracle.py
 (1M-slice SHA-256 digest of every output column, per-genome slices, the 1M
 S32 slice histogram), so this script runs the oracle over the whole space and
-commits the aggregate: hist_s32_full.npz (every record + per-k tallies).
+commits the aggregate: hist_s32_full.json (tallies, key count, per-column
+SHA-256 of the sorted records) and hist_s32_full_sample.npz (every record
+whose key is 0 mod 64).
 Blocks of 2^22 indices, checkpointed so an interrupted run resumes.
 
     python tests/golden/make_s32_full.py            # ~1 h on 8 host threads
@@ -55,11 +57,35 @@ def main() -> None:
             acc.save(ck, extra=dict(done=done))
             el = time.time() - t0
             print(f"{done / n_total:7.2%}  {len(acc)} keys  {el:.0f} s", flush=True)
-    np.savez_compressed(os.path.join(HERE, "hist_s32_full.npz"), keys=acc.keys, det=acc.det, steric=acc.steric,
-                        rep_det=acc.rep_det, rep_any=acc.rep_any, w=acc.w, h=acc.h, cells=acc.cells,
-                        shape=acc.shape, tallies=acc.tallies)
-    print("tallies", acc.tallies.tolist(), "keys", len(acc))
+    finalize(acc)
+
+
+def finalize(acc) -> None:
+    """Compact fixtures (the full record set is ~40 MB): per-column SHA-256 of the
+    sorted records (shape words [:, :5], the d=19 maximum), the tallies, and every
+    record whose key is 0 mod 64 in full."""
+    import hashlib
+    import json
+
+    def sha(a):
+        return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+    cols = dict(keys=acc.keys.astype(np.uint32), det=acc.det.astype(np.uint64), steric=acc.steric.astype(np.uint64),
+                rep_det=acc.rep_det.astype(np.uint64), rep_any=acc.rep_any.astype(np.uint64),
+                w=acc.w.astype(np.uint8), h=acc.h.astype(np.uint8), cells=acc.cells.astype(np.uint16),
+                shape=np.ascontiguousarray(acc.shape[:, :5]).astype(np.uint64))
+    meta = dict(space="s32_3_8", n=int(acc.tallies[0].sum()), ks=list(KS), hist_k=HIST_K, d=19, seed=0, strict=True,
+                n_keys=len(acc), tallies=acc.tallies.tolist(), sha256={k: sha(v) for k, v in cols.items()},
+                note="oracle/tv_oracle.c over all 2^32 indices, aggregated with classify.Histogram.from_rows")
+    with open(os.path.join(HERE, "hist_s32_full.json"), "w") as f:
+        json.dump(meta, f, indent=1)
+    sel = (acc.keys % 64) == 0
+    np.savez_compressed(os.path.join(HERE, "hist_s32_full_sample.npz"), **{k: v[sel] for k, v in cols.items()})
+    print("tallies", acc.tallies.tolist(), "keys", len(acc), "sampled", int(sel.sum()))
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "--finalize":  # from the checkpoint of a finished run
+        finalize(Histogram.load(os.environ.get("S32_CKPT", "/tmp/s32_full.ckpt"))[0])
+    else:
+        main()

@@ -85,3 +85,66 @@ def test_histogram_merge_commutative_associative():
     full = _hist_of(c, np.arange(n))
     assert Histogram.merge_many(parts) == full
     assert parts[0].merge(parts[1]).merge(parts[2]) == parts[2].merge(parts[0].merge(parts[1]))
+
+
+def _collision_rows():
+    """Synthetic per-genome rows: hash 0xABC carried by two different shapes (a 32-bit
+    collision), genome 7 (lowest index) holds shape A, genomes 9 and 12 shape B."""
+    idx = np.array([12, 9, 7, 3], np.uint64)
+    cls = np.array([[0], [2], [0], [1]], np.uint8)
+    hsh = np.array([0xABC, 0xABC, 0xABC, 0], np.uint32)
+    w = np.array([2, 2, 1, 0], np.uint8)
+    h = np.array([1, 1, 3, 0], np.uint8)
+    cells = np.array([2, 2, 3, 0], np.uint16)
+    shape = np.zeros((4, 5), np.uint64)
+    shape[[0, 1], 0] = 3
+    shape[2, 0] = 7
+    return idx, cls, hsh, w, h, cells, shape
+
+
+def test_payload_is_the_representatives():
+    """Payload (w, h, cells, bitmap) of a key = that of its lowest-index genome, whatever
+    the row order or merge order (the device histogram follows the same rule)."""
+    from paper_2205_15311_b200.classify import Histogram
+    idx, cls, hsh, w, h, cells, shape = _collision_rows()
+    for perm in ([0, 1, 2, 3], [2, 3, 1, 0], [3, 0, 2, 1]):
+        H = Histogram.from_rows(idx[perm], cls[perm], hsh[perm], w[perm], h[perm], cells[perm], shape[perm], (1,), 1)
+        assert H.keys.tolist() == [0xABC] and int(H.rep_any[0]) == 7
+        assert (int(H.w[0]), int(H.h[0]), int(H.cells[0]), int(H.shape[0, 0])) == (1, 3, 3, 7)
+    a = Histogram.from_rows(idx[:2], cls[:2], hsh[:2], w[:2], h[:2], cells[:2], shape[:2], (1,), 1)
+    b = Histogram.from_rows(idx[2:], cls[2:], hsh[2:], w[2:], h[2:], cells[2:], shape[2:], (1,), 1)
+    for m in (Histogram.merge_many([a, b]), Histogram.merge_many([b, a])):
+        assert (int(m.w[0]), int(m.cells[0]), int(m.shape[0, 0]), int(m.det[0]), int(m.steric[0])) == (1, 3, 7, 2, 1)
+
+
+def _collision_worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    from paper_2205_15311_b200.classify import Histogram
+    from paper_2205_15311_b200.distributed import allreduce_histogram
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        idx, cls, hsh, w, h, cells, shape = _collision_rows()
+        rows = [0, 1] if rank == 0 else [2, 3]  # rank 1 holds the representative (genome 7)
+        local = Histogram.from_rows(idx[rows], cls[rows], hsh[rows], w[rows], h[rows], cells[rows], shape[rows],
+                                    (1,), 1, W=5)
+        m = allreduce_histogram(local, None)
+        q.put((rank, int(m.rep_any[0]), int(m.w[0]), int(m.h[0]), int(m.cells[0]), int(m.shape[0, 0])))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_allreduce_payload_from_representative_rank():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_collision_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in res:
+        assert r[1:] == (7, 1, 3, 3, 7), r

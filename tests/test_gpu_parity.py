@@ -197,3 +197,28 @@ def test_early_unbound_cutoff_per_genome(K, early_unbound, on):
         O.classify_batch(idx, *args, 19, np.array(ks), hk, 5, strict, *[b[k] for k in G.OUT_KEYS])
         for k in G.OUT_KEYS:
             assert np.array_equal(a[k], b[k]), (args[0], ks, strict, k)
+
+
+def test_enumerate_full_s32_histogram(K):
+    """All 2^32 S^{32}_{3,8} genomes on one GPU (~10 s) against the oracle's full-space
+    aggregate (tests/golden/make_s32_full.py): tallies, key count, per-column SHA-256
+    of the sorted records, and the sampled records in full."""
+    import hashlib
+    import json
+    import os
+    from paper_2205_15311_b200.classify import enumerate_space
+    from paper_2205_15311_b200.genome import space_from_preset
+    with open(os.path.join(G.GOLDEN, "hist_s32_full.json")) as f:
+        meta = json.load(f)
+    smp = dict(np.load(os.path.join(G.GOLDEN, "hist_s32_full_sample.npz")))
+    h = enumerate_space(space_from_preset("s32_3_8"), ks=(7,), seed=0, batch_size=1 << 30, capacity=1 << 21)
+    assert h.tallies.tolist() == meta["tallies"]
+    assert len(h) == meta["n_keys"]
+    cols = dict(keys=h.keys.astype(np.uint32), det=h.det.astype(np.uint64), steric=h.steric.astype(np.uint64),
+                rep_det=h.rep_det.astype(np.uint64), rep_any=h.rep_any.astype(np.uint64), w=h.w.astype(np.uint8),
+                h=h.h.astype(np.uint8), cells=h.cells.astype(np.uint16),
+                shape=np.ascontiguousarray(h.shape[:, :5]).astype(np.uint64))
+    sel = (cols["keys"] % 64) == 0
+    for k, v in cols.items():
+        assert np.array_equal(v[sel], smp[k]), k
+        assert hashlib.sha256(np.ascontiguousarray(v).tobytes()).hexdigest() == meta["sha256"][k], k
