@@ -804,7 +804,7 @@ int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **
   e = e ? e : cudaMalloc(&P.pop0, n * 8);
   e = e ? e : cudaMalloc(&P.pop1, n * 8);
   e = e ? e : cudaMalloc(&P.cdf, n * 4);
-  e = e ? e : cudaMalloc(&P.guide, (size_t)TV_GA_BUCKETS * n * 8);
+  e = e ? e : cudaMalloc(&P.guide, (size_t)n * sizeof(ulonglong2));
   e = e ? e : cudaMalloc(&P.fstage, n * 4);
   e = e ? e : cudaMalloc(&P.tot, (size_t)h->nblocks * 8);
   e = e ? e : cudaMalloc(&P.done, 8);

@@ -6,9 +6,11 @@
 //   -- grid barrier --
 //   B. chunk offsets -> global inclusive CDF (u32) and a guide table for
 //      indexed search (Chen & Asau): the r-range [0, total) is cut into
-//      B = min(2n, total) monotone buckets b(r) = (r * M) >> 32 and guide[b] =
-//      (cdf[j], j) of the individual j owning the first r of bucket b (so most
-//      lookups need no CDF load); individual j writes the
+//      B = min(n, total) monotone buckets b(r) = (r * M) >> 32 and guide[b] =
+//      (cdf[j], j[, genome j]) of the individual j owning the first r of bucket
+//      b (so most lookups need no CDF load; for L <= 32 the CDF is packed above
+//      the genome in the population word and the guide carries the genome, so
+//      most selections are a single L2 read); individual j writes the
 //      buckets whose first r lies in its own range [cdf[j-1], cdf[j]), so the
 //      table is built in the same pass;
 //   -- grid barrier --
@@ -31,9 +33,6 @@
 #ifndef TV_GA_ILP
 #define TV_GA_ILP 2  // children per thread in flight in phase C (4 and 8 measured slower)
 #endif
-#ifndef TV_GA_BUCKETS
-#define TV_GA_BUCKETS 1  // guide buckets per individual
-#endif
 
 namespace tvb {
 
@@ -53,7 +52,8 @@ struct GaParams {
   const uint32_t *f_ext;
   uint32_t *cdf;         // n
   uint32_t *fstage;      // n: fitness staged in index order (own chunk per CTA)
-  unsigned long long *guide;  // 2n: (cdf[j] << 32) | j per bucket (first B entries used in a generation)
+  ulonglong2 *guide;     // n buckets (first B used per generation): x = (cdf[j] << 32) | j,
+                         // y = genome j (packed mode, L <= 32)
   unsigned long long *tot;  // per CTA chunk totals
   uint32_t *best;        // n_gens
   unsigned long long *sum;  // n_gens
@@ -125,10 +125,28 @@ __device__ __forceinline__ ChildDraws ga_draws(const GaParams &P, uint64_t gkey,
 // entry carries cdf[j] so a bucket whose owner covers r costs one load
 __device__ __forceinline__ uint32_t ga_pick(const GaParams &P, uint32_t r, uint32_t total, uint64_t mul) {
   if (total == 0) return r;
-  const unsigned long long e = P.guide[(uint32_t)(((uint64_t)r * mul) >> 32)];  // mul <= 2^32: no overflow
+  const unsigned long long e = P.guide[(uint32_t)(((uint64_t)r * mul) >> 32)].x;  // mul <= 2^32: no overflow
   uint32_t j = (uint32_t)e, c = (uint32_t)(e >> 32);
   while (c <= r) c = P.cdf[++j];
   return j;
+}
+
+// Packed mode (L <= 32): population words carry (cdf[j] << 32) | genome j and
+// the guide entry carries the owner's genome, so the selected parent itself is
+// returned: one L2 read when the bucket owner covers r, one more per step
+// (cdf and genome in the same word) otherwise.
+__device__ __forceinline__ uint64_t ga_pick_genome(const GaParams &P, const unsigned long long *pop, uint32_t r,
+                                                   uint32_t total, uint64_t mul) {
+  if (total == 0) return pop[r] & 0xFFFFFFFFull;
+  const ulonglong2 e = P.guide[(uint32_t)(((uint64_t)r * mul) >> 32)];
+  uint32_t j = (uint32_t)e.x, c = (uint32_t)(e.x >> 32);
+  uint64_t g = e.y;
+  while (c <= r) {
+    const unsigned long long v = pop[++j];
+    c = (uint32_t)(v >> 32);
+    g = v & 0xFFFFFFFFull;
+  }
+  return g;
 }
 
 __global__ void __launch_bounds__(1024, 1) k_ga_run(const __grid_constant__ GaParams P) {
@@ -150,14 +168,16 @@ __global__ void __launch_bounds__(1024, 1) k_ga_run(const __grid_constant__ GaPa
   int cur = 0;
   int64_t t = 0;
   // fitness of the initial population, staged in index order
+  const uint64_t full = P.L == 64 ? ~0ULL : ((1ULL << P.L) - 1);
+  const bool packed = P.L <= 32;
   for (int64_t i = c0 + tid; i < c1; i += nt)
-    P.fstage[i] = P.fitness == 0 ? (uint32_t)__popcll(P.pop0[i]) : P.f_ext[i];
+    P.fstage[i] = P.fitness == 0 ? (uint32_t)__popcll(P.pop0[i] & full) : P.f_ext[i];
+  if (tid == 0) { s_best = 0; s_cnt = 0; }
   __syncthreads();
   for (; t < P.n_gens; t++) {
     const int64_t g = P.g0 + t;
-    const unsigned long long *pop = cur ? P.pop1 : P.pop0;
+    unsigned long long *pop = cur ? P.pop1 : P.pop0;
     unsigned long long *nxt = cur ? P.pop0 : P.pop1;
-    if (tid == 0) { s_best = 0; s_cnt = 0; }
     const bool prof = P.prof && blockIdx.x == 0 && tid == 0;
     unsigned long long tp0 = prof ? ga_clock() : 0ull, tp1 = 0ull;
     // ---- A: warp sums over its segment, block scan of warp totals, stats
@@ -194,6 +214,7 @@ __global__ void __launch_bounds__(1024, 1) k_ga_run(const __grid_constant__ GaPa
     }
     __syncthreads();
     const uint32_t excl = warp_sum[wid];
+    if (tid == 0) { s_best = 0; s_cnt = 0; }  // consumed above; next written after several barriers
     grid.sync();
     if (prof) { tp1 = ga_clock(); P.prof[0] += tp1 - tp0; tp0 = tp1; }
     // ---- B: chunk offsets -> global CDF + guide table; stop decision
@@ -218,34 +239,49 @@ __global__ void __launch_bounds__(1024, 1) k_ga_run(const __grid_constant__ GaPa
     }
     __syncthreads();
     const uint32_t total = (uint32_t)s_total;
-    // bucket function b(r) = (r * mul) >> 32, monotone, B = min(2n, total) buckets
+    // bucket function b(r) = (r * mul) >> 32, monotone, B = min(n, total) buckets
     // (r < total < 2^32 and mul <= 2^32, so r * mul fits 64 bits)
-    const uint64_t nb = min((uint64_t)TV_GA_BUCKETS * (uint64_t)P.n, (uint64_t)total);
+    const uint64_t nb = min((uint64_t)P.n, (uint64_t)total);
     const uint64_t mul = total ? (nb << 32) / total : 0ull;
     if (blockIdx.x == 0 && tid == 0) P.sum[t] = s_total;
     if (s_stop) { t++; break; }
     {
       uint32_t base = (uint32_t)s_off + excl;  // inclusive CDF before this warp's current row
-      for (int k = 0; k < rows; k++) {
-        const int64_t i = s0 + k * 32 + lane;
-        const uint32_t f = i < c1 ? P.fstage[i] : 0u;
-        uint32_t x = f;
+      constexpr int RB = 4;  // rows whose loads are issued before any store (stores could alias them)
+      for (int k0 = 0; k0 < rows; k0 += RB) {
+        uint32_t fr[RB];
+        uint64_t gr[RB];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
-          if (lane >= o) x += y;
+        for (int u = 0; u < RB; u++) {
+          const int64_t i = s0 + (k0 + u) * 32 + lane;
+          const bool in = k0 + u < rows && i < c1;
+          fr[u] = in ? P.fstage[i] : 0u;
+          gr[u] = in && packed ? (pop[i] & 0xFFFFFFFFull) : 0ull;
         }
-        const uint32_t run = base + x, prev = run - f;
-        if (i < c1) {
-          P.cdf[i] = run;
-          if (f) {  // own r in [prev, run): buckets whose first r falls in it
-            const int64_t b0 = prev ? (int64_t)(((uint64_t)(prev - 1) * mul) >> 32) + 1 : 0;
-            const int64_t b1 = (int64_t)(((uint64_t)(run - 1) * mul) >> 32);
-            const unsigned long long e = ((unsigned long long)run << 32) | (uint32_t)i;
-            for (int64_t b = b0; b <= b1; b++) P.guide[b] = e;
+#pragma unroll
+        for (int u = 0; u < RB; u++) {
+          if (k0 + u >= rows) break;
+          const int64_t i = s0 + (k0 + u) * 32 + lane;
+          const uint32_t f = fr[u];
+          uint32_t x = f;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+            if (lane >= o) x += y;
           }
+          const uint32_t run = base + x, prev = run - f;
+          if (i < c1) {
+            if (packed) pop[i] = ((unsigned long long)run << 32) | gr[u];
+            else P.cdf[i] = run;
+            if (f) {  // own r in [prev, run): buckets whose first r falls in it
+              const int64_t b0 = prev ? (int64_t)(((uint64_t)(prev - 1) * mul) >> 32) + 1 : 0;
+              const int64_t b1 = (int64_t)(((uint64_t)(run - 1) * mul) >> 32);
+              const ulonglong2 e = make_ulonglong2(((unsigned long long)run << 32) | (uint32_t)i, gr[u]);
+              for (int64_t b = b0; b <= b1; b++) P.guide[b] = e;
+            }
+          }
+          base = __shfl_sync(0xFFFFFFFFu, run, 31);
         }
-        base = __shfl_sync(0xFFFFFFFFu, run, 31);
       }
     }
     grid.sync();
@@ -254,27 +290,36 @@ __global__ void __launch_bounds__(1024, 1) k_ga_run(const __grid_constant__ GaPa
     // ---- C: children, TV_GA_ILP at a time (draws first, then the dependent loads);
     //      the next generation's fitness is staged as the children are made
     constexpr int NI = TV_GA_ILP;
-    const uint64_t full = P.L == 64 ? ~0ULL : ((1ULL << P.L) - 1);
     for (int64_t i = c0 + tid; i < c1; i += NI * nt) {
       ChildDraws D[NI];
-      uint32_t pa[NI], pb[NI];
 #pragma unroll
       for (int u = 0; u < NI; u++) {
         const int64_t iu = i + u * nt;
         D[u] = iu < c1 ? ga_draws(P, gkey, iu, total) : D[0];
       }
-#pragma unroll
-      for (int u = 0; u < NI; u++) pa[u] = ga_pick(P, D[u].ra, total, mul);
-      if (P.mode != 0) {
-#pragma unroll
-        for (int u = 0; u < NI; u++) pb[u] = ga_pick(P, D[u].rb, total, mul);
-      }
       uint64_t cv[NI];
+      if (packed) {
 #pragma unroll
-      for (int u = 0; u < NI; u++) cv[u] = pop[pa[u]];
-      if (P.mode != 0) {
+        for (int u = 0; u < NI; u++) cv[u] = ga_pick_genome(P, pop, D[u].ra, total, mul);
+        if (P.mode != 0) {
 #pragma unroll
-        for (int u = 0; u < NI; u++) cv[u] = (cv[u] & D[u].top) | (pop[pb[u]] & ~D[u].top);
+          for (int u = 0; u < NI; u++)
+            cv[u] = (cv[u] & D[u].top) | (ga_pick_genome(P, pop, D[u].rb, total, mul) & ~D[u].top);
+        }
+      } else {
+        uint32_t pa[NI], pb[NI];
+#pragma unroll
+        for (int u = 0; u < NI; u++) pa[u] = ga_pick(P, D[u].ra, total, mul);
+        if (P.mode != 0) {
+#pragma unroll
+          for (int u = 0; u < NI; u++) pb[u] = ga_pick(P, D[u].rb, total, mul);
+        }
+#pragma unroll
+        for (int u = 0; u < NI; u++) cv[u] = pop[pa[u]];
+        if (P.mode != 0) {
+#pragma unroll
+          for (int u = 0; u < NI; u++) cv[u] = (cv[u] & D[u].top) | (pop[pb[u]] & ~D[u].top);
+        }
       }
 #pragma unroll
       for (int u = 0; u < NI; u++) {
