@@ -221,7 +221,7 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
       // 2^24 block: 42.7 -> 45.5 ms).  TV_EARLY_UNBOUND=0/1 forces it off/on.
       const char *eu = getenv("TV_EARLY_UNBOUND");
       P.tf_flags = nullptr;
-      if (eu ? atoi(eu) != 0 : P.a <= 2) {
+      if (!P.pay_mode && (eu ? atoi(eu) != 0 : P.a <= 2)) {
         uint32_t *flags;
         const int64_t nw = (P.n + 31) / 32;
         CK(S.get(&flags, (size_t)nw));
@@ -315,7 +315,7 @@ bool same_enumeration(const ClassifyParams &a, const ClassifyParams &b) {
 }
 
 // Fill the payload of every slot whose payload is not its representative's
-// (tv_hist.cuh): re-classify those representatives (classify mode, one call).
+// (tv_hist.cuh): replay those representatives' runs until one reproduces the key.
 int fix_payloads(tv_hist *h, cudaStream_t st) {
   const HistDev &H = h->H;
   Scratch S(st);
@@ -326,9 +326,10 @@ int fix_payloads(tv_hist *h, cudaStream_t st) {
   CK(cudaMemcpyAsync(&nkeys, H.n_keys, 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (nkeys == 0) return 0;
-  CK(S.get(&cnt, 2)); CK(S.get(&slots, nkeys)); CK(S.get(&idx, nkeys));
+  uint32_t *keys;
+  CK(S.get(&cnt, 2)); CK(S.get(&slots, nkeys)); CK(S.get(&idx, nkeys)); CK(S.get(&keys, nkeys));
   CK(cudaMemsetAsync(cnt, 0, 8, st));
-  k_hist_stale<<<256, 256, 0, st>>>(H, slots, idx, cnt);
+  k_hist_stale<<<256, 256, 0, st>>>(H, slots, idx, keys, cnt);
   CK(cudaGetLastError());
   unsigned int ns = 0;
   CK(cudaMemcpyAsync(&ns, cnt, 4, cudaMemcpyDeviceToHost, st));
@@ -337,10 +338,15 @@ int fix_payloads(tv_hist *h, cudaStream_t st) {
   if (!h->has_params)
     return fail(TV_ERR_ARG, "%u histogram records lack their representative's payload and no enumeration "
                             "parameters are known (merge complete records or enumerate into this histogram)", ns);
+  // Fast spaces: payload mode (replay the representative's runs until one reproduces
+  // the key, usually run 0).  Others: full classification of the representative,
+  // whose attributed row is the payload.
   Common C = h->params;
   ClassifyParams &P = C.P;
   P.hist_mode = 0; P.fit_mode = 0; P.indices = reinterpret_cast<const uint64_t *>(idx); P.n = ns;
   P.start = 0; P.chunk = 0; P.stride = 0;
+  P.pay_mode = C.fast ? 1 : 0;
+  P.pay_key = keys;
   uint8_t *cls, *w, *hh; uint32_t *hash; uint16_t *cells; unsigned long long *shape;
   CK(S.get(&cls, (size_t)ns * P.q)); CK(S.get(&hash, ns)); CK(S.get(&w, ns)); CK(S.get(&hh, ns));
   CK(S.get(&cells, ns)); CK(S.get(&shape, (size_t)ns * H.W));

@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(TV_FAST_MAXT, TV_FAST_MINB) k_classify_fast(co
   int minr = 0, maxr = 0, minc = 0, maxc = 0;
   int trivial_at = -1, first_unbound = -1, first_mismatch = -1;
   uint32_t hash0 = 0, best = 0, fit0 = 0;
+  int64_t pslot = -1;  // histogram slot whose payload the claiming genome's replay writes
   bool tfree = false;  // no run of this genome can go TRIVIAL (k_trivial_flags)
   Cand<A, STRICT> K;
 
@@ -301,9 +302,9 @@ __global__ void __launch_bounds__(TV_FAST_MAXT, TV_FAST_MINB) k_classify_fast(co
         if (ended == RUN_BOUNDED) {
           unsigned long long *out = nullptr;
           int64_t W = 0;
-          if (replay) {  // classify mode only (histogram payloads are filled at export)
-            out = P.out_shape + item * P.W;
-            W = P.W;
+          if (replay || P.pay_mode) {
+            out = P.hist_mode ? P.hist.shape + pslot * P.hist.W : P.out_shape + item * P.W;
+            W = P.hist_mode ? P.hist.W : P.W;
           }
           w = maxc - minc + 1;
           h = maxr - minr + 1;
@@ -342,9 +343,27 @@ __global__ void __launch_bounds__(TV_FAST_MAXT, TV_FAST_MINB) k_classify_fast(co
           for (int wi = lo; wi <= hi; wi++) Ln.gw[wi * 32] = 0xFFFFFFFFu;
         }
         if (replay) {
-          P.out_hash[item] = best;
-          P.out_w[item] = (uint8_t)w; P.out_h[item] = (uint8_t)h; P.out_cells[item] = (uint16_t)n;
+          if (!P.hist_mode) {
+            P.out_hash[item] = best;
+            P.out_w[item] = (uint8_t)w; P.out_h[item] = (uint8_t)h; P.out_cells[item] = (uint16_t)n;
+          } else {  // the genome that claimed the key provides its payload (fixed at export
+                    // if a lower-index genome carries the same key, tv_hist.cuh)
+            P.hist.whc[pslot] = (uint32_t)w | ((uint32_t)h << 8) | ((uint32_t)n << 16);
+            P.hist.pay_idx[pslot] = idx;
+          }
           st = ST_NEED;
+        } else if (P.pay_mode) {  // representative payload: first run reproducing the key
+          const uint32_t key = P.pay_key[item];
+          if (ended == RUN_BOUNDED && hs == key) {
+            P.out_hash[item] = hs;
+            P.out_w[item] = (uint8_t)w; P.out_h[item] = (uint8_t)h; P.out_cells[item] = (uint16_t)n;
+            st = ST_NEED;
+          } else if (ended != RUN_TRIVIAL && ended != RUN_OVERFLOW && ++run < P.kmax) {
+            start = true;
+          } else {
+            P.out_hash[item] = ~key;
+            st = ST_NEED;
+          }
         } else {
           // ---- fold one run (_k:323-349)
           bool done = false;
@@ -442,8 +461,8 @@ __global__ void __launch_bounds__(TV_FAST_MAXT, TV_FAST_MINB) k_classify_fast(co
                     hist_min(&P.hist.rep_any[g], idx);
                   }
                 }
-                need_payload = false;  // counts only; the representative's payload is filled at export
-                (void)gnew;
+                need_payload = gnew;
+                pslot = g;
               }
               if (need_payload) {  // replay the attributed run to emit its bitmap
                 replay = 1;

@@ -4,8 +4,9 @@
 // det/steric genome counts, the lowest DET index and the lowest DET-or-STERIC
 // index ("representative = lowest enumeration index"), and the
 // payload (w, h, cells, cropped bitmap) of the representative rep_any: the
-// enumeration kernels only count; tv_hist_export fills the payload of every
-// slot whose pay_idx is not its rep_any by re-classifying that one genome, so
+// genome that claims a key writes its payload (pay_idx = its index) during
+// the enumeration; tv_hist_export then re-derives the payload of every slot
+// whose pay_idx is not its rep_any from that one genome, so
 // colliding shapes under one 32-bit hash resolve to the lowest index exactly
 // as the per-genome aggregation does (with ~5e5 keys in S32, distinct shapes
 // sharing a 32-bit hash are expected).

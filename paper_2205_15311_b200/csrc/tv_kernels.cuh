@@ -48,23 +48,32 @@ __global__ void __launch_bounds__(128) k_classify_generic(const __grid_constant_
       if (!P.hist_mode) { P.out_hash[item] = 0; P.out_w[item] = 0; P.out_h[item] = 0; P.out_cells[item] = 0; }
       continue;
     }
-    if (P.hist_mode) {  // count only; the representative's payload is filled at export
+    unsigned long long *dst = P.out_shape + item * P.W;
+    int64_t W = P.W, g = -1;
+    if (P.hist_mode) {  // count; the claiming genome provides the payload (fixed at export, tv_hist.cuh)
       bool gnew = false;
-      const int64_t g = hist_claim(P.hist, F.hash, gnew);
+      g = hist_claim(P.hist, F.hash, gnew);
       if (g < 0) continue;
       const bool det = hc == CLS_DET;
       atomicAdd(det ? &P.hist.det[g] : &P.hist.steric[g], 1ULL);
       if (det) hist_min(&P.hist.rep_det[g], idx);
       hist_min(&P.hist.rep_any[g], idx);
-      continue;
+      if (!gnew) continue;
+      dst = P.hist.shape + g * P.hist.W;
+      W = P.hist.W;
     }
     // replay the attributed run (identical substream) to emit its bitmap
     GRun R = g_assemble(edges, P.a, P.d, P.strict, P.seed, idx, F.attr_run, V);
     int w, h, nc;
-    g_hash_region(V, P.d, R, w, h, nc, P.out_shape + item * P.W, P.W);
+    g_hash_region(V, P.d, R, w, h, nc, dst, W);
     g_cleanup(V, R);
-    P.out_hash[item] = F.hash;
-    P.out_w[item] = (uint8_t)w; P.out_h[item] = (uint8_t)h; P.out_cells[item] = (uint16_t)nc;
+    if (!P.hist_mode) {
+      P.out_hash[item] = F.hash;
+      P.out_w[item] = (uint8_t)w; P.out_h[item] = (uint8_t)h; P.out_cells[item] = (uint16_t)nc;
+    } else {
+      P.hist.whc[g] = (uint32_t)w | ((uint32_t)h << 8) | ((uint32_t)nc << 16);
+      P.hist.pay_idx[g] = idx;
+    }
   }
 }
 
@@ -130,18 +139,20 @@ __global__ void k_hist_compact(HistDev H, uint32_t *keys_out, uint32_t *slot_out
 }
 
 // slots whose payload does not belong to their representative (rep_any)
-__global__ void k_hist_stale(HistDev H, uint32_t *slot_out, unsigned long long *idx_out, unsigned int *cnt) {
+__global__ void k_hist_stale(HistDev H, uint32_t *slot_out, unsigned long long *idx_out, uint32_t *key_out,
+                             unsigned int *cnt) {
   for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < H.cap; s += (int64_t)gridDim.x * blockDim.x) {
     if (H.keys[s] && H.pay_idx[s] != H.rep_any[s]) {
       const unsigned int p = atomicAdd(cnt, 1u);
       slot_out[p] = (uint32_t)s;
       idx_out[p] = H.rep_any[s];
+      key_out[p] = (uint32_t)H.keys[s];
     }
   }
 }
 
-// payload rows of the re-classified representatives -> their slots; a hash
-// that does not reproduce the slot key flags an error
+// payload rows of the re-classified representatives -> their slots; a row
+// whose hash does not reproduce the slot key flags an error
 __global__ void k_hist_payload(HistDev H, const uint32_t *slots, const unsigned long long *idx, int64_t n,
                                const uint32_t *hash, const uint8_t *w, const uint8_t *h, const uint16_t *cells,
                                const unsigned long long *shape, unsigned int *err) {

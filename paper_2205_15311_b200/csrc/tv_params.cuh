@@ -27,6 +27,11 @@ struct ClassifyParams {
   // histogram mode (enumerate_range): no per-genome outputs
   int32_t hist_mode;
   HistDev hist;
+  // payload mode (histogram export, fast kernel): replay runs of item i until one
+  // ends BOUNDED with hash pay_key[i]; write its hash/w/h/cells/shape row and stop
+  // (no such run: out_hash[i] = ~pay_key[i])
+  int32_t pay_mode;
+  const uint32_t *pay_key;
   // GA fitness mode (JaTAM-shape fitness): out_fit[i] =
   // d^2 - shapediff(target, run-0 grid) for genomes DET at hist_k, else 0.
   // target_rows[R] bit C = target occupancy of padded cell (R, C) (d <= 29).
