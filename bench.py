@@ -174,6 +174,15 @@ def hbm_peak() -> float:
         return 6650.0  # B200_PROFILING.md fallback
 
 
+def ga_traffic():
+    """ncu DRAM bytes per generation of k_ga_run (profiles/ncu_traffic.json), or None."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))["k_ga_run"]
+        return t["dram_bytes_read_per_generation"] + t["dram_bytes_write_per_generation"]
+    except Exception:
+        return None
+
+
 def ga_bench(args, n: int = 1 << 20, gens: int = 2000) -> dict:
     """GA generations/s at population 2^20 (BASELINE.json configs[2]): Fujiyama, L=32,
     mu*L=0.3, asexual, no early stop; one cooperative launch per call."""
@@ -208,8 +217,10 @@ def ga_bench(args, n: int = 1 << 20, gens: int = 2000) -> dict:
             "e2e": {"value": rec.generations / e2e_s, "unit": "generations/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 16, "api": "evolve.run_ga"},
             "roofline": {"bound": "hbm", "achieved": 16.0 * n * k / dev_s / 1e9, "peak": hbm_peak(), "unit": "GB/s",
-                         "frac": 16.0 * n * k / dev_s / 1e9 / hbm_peak(),
-                         "note": "16 B/individual/generation algorithmic (SURVEY 8d); working set L2-resident"},
+                         "frac": 16.0 * n * k / dev_s / 1e9 / hbm_peak(), "traffic": ga_traffic(),
+                         "note": "16 B/individual/generation algorithmic (SURVEY 8d); working set L2-resident, so "
+                                 "the binding limits are the two grid barriers per generation and dependent "
+                                 "L2 reads in selection (DESIGN.md section 6)"},
             "cpu_baseline": {"value": cg / cpu_s, "unit": "generations/s", "cores": os.cpu_count(),
                              "kind": "restatement (no reference GA exists)",
                              "sample": f"{cg} generations of 2^20 on oracle/tv_ga_oracle.c, OpenMP"}}
