@@ -1,0 +1,116 @@
+"""GPU edge cases of the C-ABI paths: empty inputs, capacity limits, parameter
+mismatches, hist_k < ks[-1] in histogram mode, device merges that bring a lower
+representative, and the last indices of the S32 space."""
+import numpy as np
+import pytest
+
+from tests import _golden as G
+
+pytestmark = pytest.mark.gpu
+
+S28_ARGS = (2, 3, np.zeros(0, np.int64), np.zeros(0, np.uint8), np.arange(23, -1, -1, dtype=np.int64))
+
+
+@pytest.fixture(scope="module")
+def M():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_2205_15311_b200 import _kernels, _lib, classify, genome
+    return _kernels, _lib, classify, genome
+
+
+def test_empty_batch_and_range(M):
+    K, L, C, Gm = M
+    out = G.fresh_outputs(0, 4)
+    K.classify_batch(np.zeros(0, np.uint64), *S28_ARGS, 19, np.array([1, 2, 4, 8]), 8, np.uint64(0), True,
+                     *[out[k] for k in G.OUT_KEYS])
+    dh = C.DeviceHistogram((1, 2, 4, 8), 8, 5, 1 << 10)
+    dh.enumerate_range(Gm.SearchSpace(2, 8), 0x123, 0, 19, 0, True)
+    h = dh.export()
+    assert len(h) == 0 and h.total == 0
+
+
+def test_histogram_capacity_overflow_raises(M):
+    K, L, C, Gm = M
+    dh = C.DeviceHistogram((1, 2, 4, 8), 8, 5, 16)  # 16 slots < 2,233 S28 phenotypes
+    dh.enumerate_range(Gm.SearchSpace(2, 8), 0, 1 << 24, 19, 0, True)
+    with pytest.raises(L.TvError):
+        dh.export()
+
+
+def test_histogram_refuses_other_parameters(M):
+    K, L, C, Gm = M
+    dh = C.DeviceHistogram((1, 2, 4, 8), 8, 5, 1 << 12)
+    sp = Gm.SearchSpace(2, 8)
+    dh.enumerate_range(sp, 0, 4096, 19, 0, True)
+    with pytest.raises(ValueError):
+        dh.enumerate_range(sp, 4096, 4096, 19, 1, True)  # different seed
+    with pytest.raises(ValueError):
+        dh.enumerate_range(sp, 4096, 4096, 19, 0, False)  # different contact rule
+    dh.clear()
+    dh.enumerate_range(sp, 4096, 4096, 19, 1, True)  # fine after clear
+    assert dh.export().total == 4096
+
+
+@pytest.mark.parametrize("ks,hist_k", [((1, 2, 4, 8), 4), ((2, 8), 2), ((8,), 8)])
+def test_histogram_mode_hist_k_below_kmax(M, ks, hist_k):
+    """Histogram = aggregation of the oracle's per-genome rows for prefix ks with hist_k < ks[-1]."""
+    from oracle import oracle as O
+    K, L, C, Gm = M
+    idx = np.arange(0x5A0000, 0x5A0000 + (1 << 16), dtype=np.uint64)
+    o = G.fresh_outputs(idx.shape[0], len(ks))
+    O.classify_batch(idx, *S28_ARGS, 19, np.array(ks), hist_k, 0, True, *[o[k] for k in G.OUT_KEYS])
+    exp = C.Histogram.from_rows(idx, *[o[k] for k in G.OUT_KEYS], ks=ks, hist_k=hist_k, W=5)
+    dh = C.DeviceHistogram(ks, hist_k, 5, 1 << 14)
+    dh.enumerate_range(Gm.SearchSpace(2, 8), int(idx[0]), idx.shape[0], 19, 0, True)
+    got = dh.export()
+    for k in ("keys", "det", "steric", "rep_det", "rep_any", "w", "h", "cells", "tallies"):
+        assert np.array_equal(getattr(got, k).astype(np.int64), getattr(exp, k).astype(np.int64)), k
+    assert np.array_equal(got.shape, exp.shape)
+
+
+def test_device_merge_lower_representative_brings_payload(M):
+    """A merged record whose rep_any is lower than the device's takes over the payload."""
+    K, L, C, Gm = M
+    sp = Gm.SearchSpace(2, 8)
+    dh = C.DeviceHistogram((1, 2, 4, 8), 8, 5, 1 << 12)
+    dh.enumerate_range(sp, 1 << 20, 1 << 16, 19, 0, True)
+    h = dh.export()
+    i = int(np.argmax(h.det))
+    fake = C.Histogram((1, 2, 4, 8), 8, 5, keys=h.keys[i:i + 1].copy(), det=np.array([1], np.uint64),
+                       steric=np.zeros(1, np.uint64), rep_det=np.array([5], np.uint64),
+                       rep_any=np.array([5], np.uint64), w=np.array([1], np.uint8), h=np.array([1], np.uint8),
+                       cells=np.array([1], np.uint16), shape=np.array([[1, 0, 0, 0, 0]], np.uint64),
+                       tallies=np.zeros((4, 5), np.int64))
+    dh.merge(fake)
+    m = dh.export()
+    j = int(np.searchsorted(m.keys, h.keys[i]))
+    assert int(m.rep_any[j]) == 5 and int(m.det[j]) == int(h.det[i]) + 1
+    assert (int(m.w[j]), int(m.h[j]), int(m.cells[j]), int(m.shape[j, 0])) == (1, 1, 1, 1)
+    # a record with a higher representative leaves the payload alone
+    dh.clear()
+    dh.enumerate_range(sp, 1 << 20, 1 << 16, 19, 0, True)
+    fake.rep_any[:] = fake.rep_det[:] = np.uint64(1 << 40)
+    dh.merge(fake)
+    m = dh.export()
+    assert (int(m.w[j]), int(m.h[j]), int(m.cells[j])) == (int(h.w[i]), int(h.h[i]), int(h.cells[i]))
+    assert np.array_equal(m.shape[j], h.shape[i])
+
+
+def test_s32_top_of_index_range_vs_oracle(M):
+    """The last 2^16 indices of S32 (index bits near 2^32) through classify_batch and the histogram."""
+    from oracle import oracle as O
+    K, L, C, Gm = M
+    sp = Gm.space_from_preset("s32_3_8")
+    a, bpl, mp, mv, fp = sp.kernel_args()
+    idx = np.arange((1 << 32) - (1 << 16), 1 << 32, dtype=np.uint64)
+    g = G.fresh_outputs(idx.shape[0], 1)
+    o = G.fresh_outputs(idx.shape[0], 1)
+    K.classify_batch(idx, a, bpl, mp, mv, fp, 19, np.array([7]), 7, np.uint64(0), True, *[g[k] for k in G.OUT_KEYS])
+    O.classify_batch(idx, a, bpl, mp, mv, fp, 19, np.array([7]), 7, 0, True, *[o[k] for k in G.OUT_KEYS])
+    for k in G.OUT_KEYS:
+        assert np.array_equal(g[k], o[k]), k
+    h = C.enumerate_space(sp, ks=(7,), start=int(idx[0]), count=idx.shape[0], batch_size=1 << 14)
+    exp = C.Histogram.from_rows(idx, *[o[k] for k in G.OUT_KEYS], ks=(7,), hist_k=7, W=5)
+    for k in ("keys", "det", "steric", "rep_det", "rep_any", "w", "h", "cells", "tallies"):
+        assert np.array_equal(getattr(h, k).astype(np.int64), getattr(exp, k).astype(np.int64)), k
