@@ -282,6 +282,49 @@ def s32_bench(args, rank: int, world: int, stream) -> dict:
             "histogram_ok": ok, "phenotypes": len(final)}
 
 
+def ga_jatam_bench(n: int = 1 << 20, gens: int = 20) -> dict:
+    """GA with JaTAM-shape fitness (BASELINE.json configs[3]): population 2^20 of S_{2,8}
+    genomes (L = 24), fitness = d^2 - shapediff(target, run-0 grid) for genomes DET at k = 8
+    (k_classify_fast fit mode over the whole population each generation), then one GA
+    generation (roulette on that fitness, asexual, muL = 0.3).  Random initial population
+    (uniform over S_{2,8}) so the timed generations classify representative genomes."""
+    import torch
+    from paper_2205_15311_b200 import assembly as A
+    from paper_2205_15311_b200 import evolve as E
+    from paper_2205_15311_b200.genome import SearchSpace, decode_tileset, genome_at_index
+    S28 = SearchSpace(2, 8)
+    tgt_idx = 0x801772  # a 12-cell deterministic S_{2,8} shape (the target of tests/test_ga.py)
+    target = A.assemble_once(decode_tileset(genome_at_index(S28, tgt_idx), S28), 19, seed=0, genome_index=tgt_idx,
+                             run_index=0).grid.cells >= 0
+    ga = E.DeviceGA(n, 24, 0.3, "asexual")
+    ga.set_population(np.random.default_rng(11).integers(0, 1 << 24, n, dtype=np.uint64))
+    stream = torch.cuda.current_stream()
+
+    def gen(g):
+        f = ga.jatam_fitness(S28, target, 19, 8)
+        return ga.run(5, g, 1, 19 * 19, n, 0, f_ext=f)
+
+    for g in range(2):
+        gen(g)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    best = 0
+    for g in range(2, 2 + gens):
+        best = max(best, int(gen(g)[1][-1]))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dev_s = e0.elapsed_time(e1) / 1e3
+    ga.close()
+    return {"metric": "GA generations/sec (JaTAM-shape fitness)", "value": gens / dev_s, "unit": "generations/s",
+            "ms_per_generation": dev_s / gens * 1e3, "genomes_classified_per_s": gens * n / dev_s,
+            "config": {"workload": "GA toward a 12-cell S_(2,8) target shape, population 2^20, L=24, k=8, d=19, "
+                                   "muL=0.3, asexual, random initial population", "generations_timed": gens},
+            "best_fitness_seen": best,
+            "note": "each generation = k_trivial_flags + k_classify_fast (fit mode) over 2^20 genomes + one "
+                    "k_ga_run generation; timed with CUDA events on the launch stream"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -432,9 +475,10 @@ def main():
         except Exception as e:  # the oracle is test infrastructure; report, do not fail the bench
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {e}"}
     s32 = None if args.no_s32 else s32_bench(args, rank, world, stream)
-    ga = None
+    ga = ga_jatam = None
     if rank == 0 and not args.no_ga:
         ga = ga_bench(args)
+        ga_jatam = ga_jatam_bench()
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
@@ -447,7 +491,7 @@ def main():
                 "e2e": {"value": N_S28 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                         "d2h_bytes_per_step": int(d2h), "api": "classify.enumerate_space"},
                 "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(),
-                "gpu_launches": 3 * args.steps, "s32": s32, "ga": ga}
+                "gpu_launches": 3 * args.steps, "s32": s32, "ga": ga, "ga_jatam": ga_jatam}
         print(json.dumps(line), flush=True)
     hist.close()
     if world > 1:

@@ -221,7 +221,8 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
       // 2^24 block: 42.7 -> 45.5 ms).  TV_EARLY_UNBOUND=0/1 forces it off/on.
       const char *eu = getenv("TV_EARLY_UNBOUND");
       P.tf_flags = nullptr;
-      if (!P.pay_mode && (eu ? atoi(eu) != 0 : P.a <= 2)) {
+      // (payload and fitness modes stop at the first UNBOUND run anyway)
+      if (!P.pay_mode && !P.fit_mode && (eu ? atoi(eu) != 0 : P.a <= 2)) {
         uint32_t *flags;
         const int64_t nw = (P.n + 31) / 32;
         CK(S.get(&flags, (size_t)nw));

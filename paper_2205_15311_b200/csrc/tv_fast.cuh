@@ -371,6 +371,7 @@ __global__ void __launch_bounds__(TV_FAST_MAXT, TV_FAST_MINB) k_classify_fast(co
             rh[run * 32] = hs;
             if (run == 0) { hash0 = hs; fit0 = (uint32_t)n | ((uint32_t)ov << 16); }
             else if (first_mismatch < 0 && first_unbound != 0 && hs != hash0) first_mismatch = run;
+            if (P.fit_mode && first_mismatch >= 0) done = true;  // not DET: fitness 0 whatever follows
           } else if (ended == RUN_UNBOUND) {
             rh[run * 32] = 0u;
             if (first_unbound < 0) {
@@ -379,6 +380,7 @@ __global__ void __launch_bounds__(TV_FAST_MAXT, TV_FAST_MINB) k_classify_fast(co
               // later run goes TRIVIAL, which the genome's flag proves impossible
               if (tfree) done = true;
             }
+            if (P.fit_mode) done = true;  // not DET: fitness 0 whatever follows
           } else {
             done = true;
             if (ended == RUN_TRIVIAL) trivial_at = run;
