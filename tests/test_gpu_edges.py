@@ -114,3 +114,23 @@ def test_s32_top_of_index_range_vs_oracle(M):
     exp = C.Histogram.from_rows(idx, *[o[k] for k in G.OUT_KEYS], ks=(7,), hist_k=7, W=5)
     for k in ("keys", "det", "steric", "rep_det", "rep_any", "w", "h", "cells", "tallies"):
         assert np.array_equal(getattr(h, k).astype(np.int64), getattr(exp, k).astype(np.int64)), k
+
+
+def test_spec_acceptance_2_s28_reference_values(M):
+    """SPEC ACCEPTANCE 2 on the device, against the reference's own S_{2,8} values recorded in
+    SURVEY.md section 0 (71 hashes with DET and STERIC genomes, steric/unbound = 0.124,
+    106 DET hashes) and the monotone misclassification (c) relative to k = 32."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "acc", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "acceptance_s28.py"))
+    acc = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(acc)
+    r = acc.run()
+    assert r["a_mixed_hashes"] == 71 and r["det_hashes"] == 106
+    assert abs(r["b_steric_over_unbound_k8"] - 0.124) < 0.0005
+    assert r["c_non_increasing"] and r["c_misclassified_det_vs_k32"]["32"] == 0.0
+    hg = G.hist_golden("s28_full")  # prefix tallies at k <= 8 equal the reference's
+    for i, k in enumerate((1, 2, 4, 8)):
+        t = r["tallies"][str(k)]
+        assert [t["det"], t["trivial"], t["steric"], t["unbound"], t["error"]] == hg["tallies"][i].tolist()
