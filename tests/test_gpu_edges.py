@@ -134,3 +134,16 @@ def test_spec_acceptance_2_s28_reference_values(M):
     for i, k in enumerate((1, 2, 4, 8)):
         t = r["tallies"][str(k)]
         assert [t["det"], t["trivial"], t["steric"], t["unbound"], t["error"]] == hg["tallies"][i].tolist()
+
+
+def test_spec_acceptance_3_s28_hash_integrity(M):
+    """No two distinct deterministic S_{2,8} shapes share a 32-bit hash (SPEC ACCEPTANCE 3)."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "hi", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "hash_integrity.py"))
+    hi = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(hi)
+    r = hi.run("s28")
+    assert r["det_payloads"] == r["det_hashes"] == 106 and r["colliding_hashes"] == 0
+    assert f"{r['collision_probability_1000'] * 100:.1g}" == "0.01"  # Eq. 2: ~0.01 % for 1000 phenotypes

@@ -1,3 +1,5 @@
+"""Time one full S_{2,8} enumeration and one 2^24 block of S32 (best of 3, host clock around a
+synchronised call); TV_LIB_PATH selects an alternate build for A/B runs."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
