@@ -147,3 +147,14 @@ def test_spec_acceptance_3_s28_hash_integrity(M):
     r = hi.run("s28")
     assert r["det_payloads"] == r["det_hashes"] == 106 and r["colliding_hashes"] == 0
     assert f"{r['collision_probability_1000'] * 100:.1g}" == "0.01"  # Eq. 2: ~0.01 % for 1000 phenotypes
+
+
+def test_spec_acceptance_7_csv_byte_identical(M):
+    """Same (seed, k, d, space) with different batch sizes and chunk orders -> byte-identical CSV."""
+    K, L, C, Gm = M
+    sp = Gm.SearchSpace(2, 8)
+    a = C.enumerate_space(sp, ks=(1, 2, 4, 8), start=0x300000, count=1 << 19, batch_size=1 << 19).to_csv()
+    b = C.enumerate_space(sp, ks=(1, 2, 4, 8), start=0x300000, count=1 << 19, batch_size=12345).to_csv()
+    plan = C.chunk_plan(0x300000, 1 << 19, 1 << 15)[::-1]  # reversed chunk order
+    c = C.enumerate_space(sp, ks=(1, 2, 4, 8), start=0x300000, count=1 << 19, chunks=plan).to_csv()
+    assert a.encode() == b.encode() == c.encode()
