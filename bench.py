@@ -274,12 +274,30 @@ def s32_bench(args, rank: int, world: int, stream) -> dict:
         ok = final.tallies.tolist() == gold["tallies"] and len(final) == gold["n_keys"]
     except FileNotFoundError:
         ok = None
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:  # the pinned C port on all host threads, 64 evenly spaced 2^16-index blocks of S32
+            from oracle import oracle as O
+            idx = (np.arange(64, dtype=np.uint64)[:, None] * np.uint64(n_all // 64)
+                   + np.arange(1 << 16, dtype=np.uint64)[None, :]).reshape(-1)
+            m = idx.shape[0]
+            outs = [np.zeros((m, 1), np.uint8), np.zeros(m, np.uint32), np.zeros(m, np.uint8), np.zeros(m, np.uint8),
+                    np.zeros(m, np.uint16), np.zeros((m, 6), np.uint64)]
+            O.classify_batch(idx[:4096], a, bpl, mp, mv, fp, 19, ks, 7, 0, True, *[o[:4096] for o in outs])
+            t = time.perf_counter()
+            O.classify_batch(idx, a, bpl, mp, mv, fp, 19, ks, 7, 0, True, *outs)
+            dt = time.perf_counter() - t
+            cpu = {"value": m / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"64 evenly spaced blocks x 65536 indices of S^32_(3,8) ({m} genomes, {dt:.2f} s); "
+                             "oracle/tv_oracle.c, OpenMP all host threads"}
+        except Exception as e:
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {e}"}
     return {"metric": "genotypes classified/sec, full S^{32}_{3,8}", "value": n_all / (ms / 1e3), "unit": UNIT,
             "ms": ms, "n_gpus": world, "scaling": "strong",
             "config": {"workload": "full S^32_(3,8) enumeration: 2^32 genomes -> phenotype histogram", "ks": [7],
                        "hist_k": 7, "d": 19, "seed": 0, "strict": True, "chunking": f"{chunk} round-robin",
                        "timed": "one pass after a 2^24 warm-up chunk (inputs are index ranges; no L2 reuse)"},
-            "histogram_ok": ok, "phenotypes": len(final)}
+            "histogram_ok": ok, "phenotypes": len(final), "cpu_baseline": cpu}
 
 
 def ga_jatam_bench(n: int = 1 << 20, gens: int = 20) -> dict:
