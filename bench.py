@@ -343,6 +343,31 @@ def ga_jatam_bench(n: int = 1 << 20, gens: int = 20) -> dict:
                     "k_ga_run generation; timed with CUDA events on the launch stream"}
 
 
+def ga_sweep_bench(runs: int = 100) -> dict:
+    """Paper-scale sweep point (Figs. 9-10: N = 512, L = 32, muL = 0.3, 100 runs x 20000
+    generations, no early stop) as ONE replica launch (tv_ga_replicas), against one
+    single-run launch of the same configuration for the sequential rate."""
+    import torch
+    from paper_2205_15311_b200 import evolve as E
+    cfg = E.GAConfig(mu_L=0.3, stop_when="never")
+    E.run_replicas(E.GAConfig(cutoff=100, stop_when="never"), [0, 1])
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    recs = E.run_replicas(cfg, range(runs))
+    el = time.perf_counter() - t
+    t = time.perf_counter()
+    one = E.run_ga(cfg, seed=0)
+    el1 = time.perf_counter() - t
+    gens = sum(r.generations for r in recs)
+    return {"metric": "GA sweep replica-generations/sec", "value": gens / el, "unit": "generations/s",
+            "config": {"workload": "Fujiyama GA sweep point: 100 runs x 20000 generations, N=512, L=32, muL=0.3, "
+                                   "asexual, roulette", "runs": runs},
+            "seconds": el, "single_run_generations_per_s": one.generations / el1,
+            "speedup_vs_sequential_runs": el1 * runs / el,
+            "note": "host clock around the public API call (evolve.run_replicas): includes the launch and "
+                    "the D2H copy of every run's per-generation records; record r == run_ga(seed=r)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -493,10 +518,11 @@ def main():
         except Exception as e:  # the oracle is test infrastructure; report, do not fail the bench
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {e}"}
     s32 = None if args.no_s32 else s32_bench(args, rank, world, stream)
-    ga = ga_jatam = None
+    ga = ga_jatam = ga_sweep = None
     if rank == 0 and not args.no_ga:
         ga = ga_bench(args)
         ga_jatam = ga_jatam_bench()
+        ga_sweep = ga_sweep_bench()
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
@@ -509,7 +535,8 @@ def main():
                 "e2e": {"value": N_S28 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                         "d2h_bytes_per_step": int(d2h), "api": "classify.enumerate_space"},
                 "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(),
-                "gpu_launches": 3 * args.steps, "s32": s32, "ga": ga, "ga_jatam": ga_jatam}
+                "gpu_launches": 3 * args.steps, "s32": s32, "ga": ga, "ga_jatam": ga_jatam,
+                "ga_sweep": ga_sweep}
         print(json.dumps(line), flush=True)
     hist.close()
     if world > 1:

@@ -165,6 +165,16 @@ int tv_ga_population_ptr(tv_ga *h, uint64_t **dev_ptr);
  * stats best/sum/count(f >= target) [h|d] (may be NULL), stop after recording
  * a generation with count >= 1 (stop_when 1) or >= adapt_count (2), else
  * reproduce.  *gens_done = generations evaluated.  Synchronises. */
+/* R independent GA runs (SPEC.md:415-432 sweeps) in one launch, one CTA per run with
+ * the population in shared memory (n <= 8192).  Run r is bit-identical to
+ * tv_ga_run with seed seeds[r] from the same initial population (init [h|d]
+ * R x n, NULL = all zero).  Outputs [h|d]: done/disc/adapt int64[R] (disc/adapt
+ * = first generation with count >= 1 / >= adapt_count, else -1); optional
+ * best/sum/count [R x n_gens] and final_pop [R x n]. */
+int tv_ga_replicas(int64_t n, int32_t L, int32_t mode, const uint64_t *T, int32_t R, const uint64_t *seeds,
+                   const uint64_t *init, int64_t g0, int64_t n_gens, uint32_t target, int64_t adapt_count,
+                   int32_t stop_when, int64_t *done, int64_t *disc, int64_t *adapt, uint32_t *best, uint64_t *sum,
+                   uint32_t *count, uint64_t *final_pop, void *stream);
 int tv_ga_run(tv_ga *h, uint64_t seed, int64_t g0, int64_t n_gens, uint32_t target, int64_t adapt_count,
               int32_t stop_when, const uint32_t *f_ext, uint32_t *best, uint64_t *sum, uint32_t *count,
               int64_t *gens_done, void *stream);

@@ -71,6 +71,8 @@ _SIGS = {
     "tv_ga_get_population": (_i32, [_p, _p, _p]),
     "tv_ga_population_ptr": (_i32, [_p, ctypes.POINTER(_p)]),
     "tv_ga_run": (_i32, [_p, _u64, _i64, _i64, ctypes.c_uint32, _i64, _i32, _p, _p, _p, _p, _p, _p]),
+    "tv_ga_replicas": (_i32, [_i64, _i32, _i32, _p, _i32, _p, _p, _i64, _i64, ctypes.c_uint32, _i64, _i32, _p, _p, _p,
+                              _p, _p, _p, _p, _p]),
     "tv_ga_fitness_jatam": (_i32, [_p, _i32, _i32, _p, _p, _i64, _p, _i64, _i32, _i32, _u64, _i32, _p, _p, _p]),
     "tv_int_peak_launch": (_i32, [_i64, _i32, _i32, _p, _p]),
     "tv_sm_count": (_i32, [_p]),

@@ -905,6 +905,63 @@ int tv_ga_run(tv_ga *h, uint64_t seed, int64_t g0, int64_t n_gens, uint32_t targ
   return 0;
 }
 
+int tv_ga_replicas(int64_t n, int32_t L, int32_t mode, const uint64_t *T, int32_t R, const uint64_t *seeds,
+                   const uint64_t *init, int64_t g0, int64_t n_gens, uint32_t target, int64_t adapt_count,
+                   int32_t stop_when, int64_t *done, int64_t *disc, int64_t *adapt, uint32_t *best, uint64_t *sum,
+                   uint32_t *count, uint64_t *final_pop, void *stream) {
+  if (n < 2 || n > 8192) return fail(TV_ERR_ARG, "replica population %lld outside [2, 8192]", (long long)n);
+  if (L < 1 || L > 64) return fail(TV_ERR_ARG, "genome length %d outside [1, 64]", L);
+  if (mode < 0 || mode > 2) return fail(TV_ERR_ARG, "reproduction mode %d not in {0,1,2}", mode);
+  if (R < 1) return fail(TV_ERR_ARG, "need at least one replica");
+  if (n_gens < 1) return fail(TV_ERR_ARG, "n_gens must be >= 1");
+  if (stop_when < 0 || stop_when > 2) return fail(TV_ERR_ARG, "stop_when %d not in {0,1,2}", stop_when);
+  if (!seeds || !done || !disc || !adapt) return fail(TV_ERR_ARG, "seeds, done, disc and adapt are required");
+  int dev;
+  if (int rc = current_device(&dev)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  GaRepParams Q;
+  memset(&Q, 0, sizeof Q);
+  GaParams &P = Q.G;
+  P.n = n; P.L = L; P.mode = mode; P.target = target; P.adapt_count = adapt_count; P.stop_when = stop_when;
+  P.g0 = g0; P.n_gens = n_gens;
+  for (int j = 0; j < 64; j++) P.T[j] = j < L ? T[j] : ~0ULL;
+  Q.R = R;
+  const size_t gens = (size_t)R * (size_t)n_gens;
+  {
+    Scratch S(st);
+    uint64_t *d_seeds, *d_init = nullptr, *d_fin = nullptr, *d_sum = nullptr;
+    int64_t *d_done, *d_disc, *d_adapt;
+    uint32_t *d_best = nullptr, *d_count = nullptr;
+    bool hs, hi = false;
+    if (int rc = stage_in(seeds, (size_t)R, true, S, &d_seeds, hs)) return rc;
+    if (init) if (int rc = stage_in(init, (size_t)R * n, true, S, &d_init, hi)) return rc;
+    CK(S.get(&d_done, R)); CK(S.get(&d_disc, R)); CK(S.get(&d_adapt, R));
+    if (best) CK(S.get(&d_best, gens));
+    if (sum) CK(S.get(&d_sum, gens));
+    if (count) CK(S.get(&d_count, gens));
+    if (final_pop) CK(S.get(&d_fin, (size_t)R * n));
+    Q.seeds = d_seeds; Q.init = reinterpret_cast<const unsigned long long *>(d_init);
+    Q.final_pop = reinterpret_cast<unsigned long long *>(d_fin);
+    Q.done = d_done; Q.disc = d_disc; Q.adapt = d_adapt;
+    Q.best = d_best; Q.sum = reinterpret_cast<unsigned long long *>(d_sum); Q.count = d_count;
+    const int threads = (int)std::min<int64_t>(1024, (n + 31) / 32 * 32);
+    const size_t smem = (size_t)n * (2 * 8 + 4);
+    CK(cudaFuncSetAttribute((const void *)k_ga_replicas, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    void *args[] = {&Q};
+    CK(cudaLaunchKernel((const void *)k_ga_replicas, dim3((unsigned)R), dim3(threads), args, smem, st));
+    g_launch[0] = 3; g_launch[1] = R; g_launch[2] = threads; g_launch[3] = (int64_t)smem; g_launch[4] = 1;
+    CK(cudaMemcpyAsync(done, d_done, (size_t)R * 8, cudaMemcpyDefault, st));
+    CK(cudaMemcpyAsync(disc, d_disc, (size_t)R * 8, cudaMemcpyDefault, st));
+    CK(cudaMemcpyAsync(adapt, d_adapt, (size_t)R * 8, cudaMemcpyDefault, st));
+    if (best) CK(cudaMemcpyAsync(best, d_best, gens * 4, cudaMemcpyDefault, st));
+    if (sum) CK(cudaMemcpyAsync(sum, d_sum, gens * 8, cudaMemcpyDefault, st));
+    if (count) CK(cudaMemcpyAsync(count, d_count, gens * 4, cudaMemcpyDefault, st));
+    if (final_pop) CK(cudaMemcpyAsync(final_pop, d_fin, (size_t)R * n * 8, cudaMemcpyDefault, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
 int tv_ga_fitness_jatam(tv_ga *h, int32_t a, int32_t bpl, const int64_t *mask_pos, const uint8_t *mask_val,
                         int64_t m, const int64_t *free_pos, int64_t nfree, int32_t d, int32_t k, uint64_t seed,
                         int32_t strict, const uint8_t *target_occ, uint32_t *f_out, void *stream) {

@@ -342,3 +342,136 @@ __global__ void __launch_bounds__(1024, 1) k_ga_run(const __grid_constant__ GaPa
 }
 
 }  // namespace tvb
+
+namespace tvb {
+
+// ---------------------------------------------------------------------------
+// Replica GA: R independent runs (SPEC:415-432 sweeps, Figs. 9-10 at N = 512),
+// one CTA per replica with its population, CDF and statistics in shared
+// memory, so a generation needs only block barriers -- no grid barrier.
+// Replica r uses seed seeds[r] and is bit-identical to k_ga_run (and to
+// oracle/tv_ga_oracle.c) with that seed: same draws (ga_draws), same
+// selection (first j with cdf[j] > r), same stop rule (stats of generation t
+// are taken before reproduction; a met stop condition ends the run there).
+struct GaRepParams {
+  GaParams G;            // n, L, mode, target, adapt_count, stop_when, g0, n_gens, T (per-replica seed below)
+  int32_t R;
+  const uint64_t *seeds;                 // R
+  const unsigned long long *init;        // R x n initial genomes, or nullptr (all zero)
+  unsigned long long *final_pop;         // R x n, or nullptr
+  int64_t *done;                         // R: generations evaluated
+  int64_t *disc;                         // R: first generation with count >= 1, else -1
+  int64_t *adapt;                        // R: first generation with count >= adapt_count, else -1
+  uint32_t *best;                        // R x n_gens, or nullptr
+  unsigned long long *sum;               // R x n_gens, or nullptr
+  uint32_t *count;                       // R x n_gens, or nullptr
+};
+
+__global__ void __launch_bounds__(1024, 1) k_ga_replicas(const __grid_constant__ GaRepParams Q) {
+  extern __shared__ unsigned long long rsm[];
+  const GaParams &P = Q.G;
+  const int rep = blockIdx.x;
+  if (rep >= Q.R) return;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  const int n = (int)P.n;
+  unsigned long long *popA = rsm, *popB = rsm + n;
+  uint32_t *cdf = reinterpret_cast<uint32_t *>(rsm + 2 * n);
+  __shared__ uint32_t w_sum[32], w_best[32], w_cnt[32];
+  __shared__ uint32_t s_total;
+  __shared__ int s_stop;
+  const uint64_t full = P.L == 64 ? ~0ULL : ((1ULL << P.L) - 1);
+  const uint64_t seed = Q.seeds[rep];
+  for (int i = tid; i < n; i += nt) popA[i] = Q.init ? (Q.init[(int64_t)rep * n + i] & full) : 0ull;
+  int64_t disc = -1, adap = -1, t = 0;  // disc/adap tracked by thread 31 (it sees the stats)
+  int cur = 0;
+  __syncthreads();
+  for (; t < P.n_gens; t++) {
+    unsigned long long *pop = cur ? popB : popA, *nxt = cur ? popA : popB;
+    // fitness + inclusive CDF over the population (index order), stats
+    // each thread owns a contiguous run of individuals; warp scan of the run totals
+    const int per = (n + nt - 1) / nt, i0 = min(n, tid * per), i1 = min(n, i0 + per);
+    uint32_t acc = 0, best = 0, cnt = 0;
+    for (int i = i0; i < i1; i++) {
+      const uint32_t f = (uint32_t)__popcll(pop[i]);
+      acc += f;
+      best = max(best, f);
+      cnt += f >= P.target;
+    }
+    uint32_t x = acc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+      if (lane >= o) x += y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      best = max(best, __shfl_xor_sync(0xFFFFFFFFu, best, o));
+      cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
+    }
+    if (lane == 31) w_sum[wid] = x;
+    if (lane == 0) { w_best[wid] = best; w_cnt[wid] = cnt; }
+    __syncthreads();
+    if (wid == 0) {
+      const uint32_t v = lane < nw ? w_sum[lane] : 0u;
+      uint32_t s = v, b = lane < nw ? w_best[lane] : 0u, q = lane < nw ? w_cnt[lane] : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, s, o);
+        if (lane >= o) s += y;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        b = max(b, __shfl_xor_sync(0xFFFFFFFFu, b, o));
+        q += __shfl_xor_sync(0xFFFFFFFFu, q, o);
+      }
+      w_sum[lane] = s - v;  // exclusive warp offsets
+      if (lane == 31) {
+        s_total = s;
+        const int64_t gi = (int64_t)rep * P.n_gens + t;
+        if (Q.best) Q.best[gi] = b;
+        if (Q.sum) Q.sum[gi] = s;
+        if (Q.count) Q.count[gi] = q;
+        if (disc < 0 && q >= 1u) disc = t;
+        if (adap < 0 && (int64_t)q >= P.adapt_count) adap = t;
+        s_stop = (P.stop_when == 1 && q >= 1u) || (P.stop_when == 2 && (int64_t)q >= P.adapt_count);
+      }
+    }
+    __syncthreads();
+    {
+      uint32_t run = w_sum[wid] + x - acc;
+      for (int i = i0; i < i1; i++) {
+        run += (uint32_t)__popcll(pop[i]);
+        cdf[i] = run;
+      }
+    }
+    const uint32_t total = s_total;
+    if (s_stop) { t++; break; }
+    __syncthreads();
+    const uint64_t gkey = mix64(seed ^ (kGold * ((uint64_t)(P.g0 + t) + 1)));
+    for (int i = tid; i < n; i += nt) {
+      const ChildDraws D = ga_draws(P, gkey, i, total);
+      auto pick = [&](uint32_t r) -> uint32_t {
+        if (total == 0) return r;
+        int lo = 0, hi = n - 1;  // first j with cdf[j] > r (cdf[n-1] = total > r)
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (cdf[mid] > r) hi = mid; else lo = mid + 1;
+        }
+        return (uint32_t)lo;
+      };
+      uint64_t c = pop[pick(D.ra)];
+      if (P.mode != 0) c = (c & D.top) | (pop[pick(D.rb)] & ~D.top);
+      nxt[i] = (c ^ D.flips) & full;
+    }
+    cur ^= 1;
+    __syncthreads();
+  }
+  if (tid == 31) { Q.done[rep] = t; Q.disc[rep] = disc; Q.adapt[rep] = adap; }
+  if (Q.final_pop) {  // a stopped run keeps the population it was evaluated on (as k_ga_run)
+    __syncthreads();
+    const unsigned long long *fin = cur ? popB : popA;
+    for (int i = tid; i < n; i += nt) Q.final_pop[(int64_t)rep * n + i] = fin[i];
+  }
+}
+
+}  // namespace tvb

@@ -319,6 +319,43 @@ def run_ga(cfg: GAConfig, fitness="fujiyama", seed: int = 0, chunk: int = 4096) 
                      int(adap[0]) if adap.size else None, cfg, seed)
 
 
+REPLICA_MAX_POP = 8192
+
+
+def run_replicas(cfg: GAConfig, seeds) -> list[RunRecord]:
+    """Independent Fujiyama runs, one per seed, in ONE device launch (tv_ga_replicas: a
+    CTA per run, population in shared memory, block barriers only).  Record r is
+    identical to ``run_ga(cfg, seed=seeds[r])``.  Needs cfg.pop_size <= 8192."""
+    seeds = np.ascontiguousarray([int(x) for x in seeds], np.uint64)
+    R, n, L = seeds.shape[0], int(cfg.pop_size), int(cfg.length)
+    if R == 0:
+        return []
+    if n > REPLICA_MAX_POP:
+        raise ValueError(f"replica runs hold the population in shared memory: pop_size <= {REPLICA_MAX_POP}")
+    T = poisson_thresholds(cfg.mu_L, L)
+    adapt_count = math.ceil(cfg.adapt_fraction * n)
+    stop = {"never": 0, "discovery": 1, "adaptation": 2}[cfg.stop_when]
+    n_gens = int(cfg.cutoff)
+    init = None
+    if cfg.init is not None:
+        init = np.ascontiguousarray(np.broadcast_to(np.asarray(cfg.init, np.uint64), (R, n)))
+    done, disc, adap = (np.zeros(R, np.int64) for _ in range(3))
+    best = np.zeros((R, n_gens), np.uint32)
+    sm = np.zeros((R, n_gens), np.uint64)
+    cnt = np.zeros((R, n_gens), np.uint32)
+    P = _lib.ptr
+    _lib.check(_lib.lib().tv_ga_replicas(n, L, MODES[cfg.mode], P(T), R, P(seeds), P(init), 0, n_gens, int(cfg.target),
+                                         adapt_count, stop, P(done), P(disc), P(adap), P(best), P(sm), P(cnt), None,
+                                         None))
+    out = []
+    for r in range(R):
+        k = int(done[r])
+        out.append(RunRecord(best[r, :k].copy(), sm[r, :k].astype(np.float64) / n, cnt[r, :k].copy(), k,
+                             int(disc[r]) if disc[r] >= 0 else None, int(adap[r]) if adap[r] >= 0 else None,
+                             cfg, int(seeds[r])))
+    return out
+
+
 def sweep(mu_L_grid, runs: int = 100, base: GAConfig | None = None, seed0: int = 0, sample_size: int = 100,
           resamples: int = 10000) -> list[dict]:
     """SPEC:452 sweep JSON rows: {muL, runs, discovery:{median, ci_lo, ci_hi, censored}, adaptation:{...}}."""
@@ -326,7 +363,9 @@ def sweep(mu_L_grid, runs: int = 100, base: GAConfig | None = None, seed0: int =
     rows = []
     for mu in mu_L_grid:
         cfg = GAConfig(**{**base.__dict__, "mu_L": float(mu)})
-        recs = [run_ga(cfg, seed=seed0 + r) for r in range(runs)]
+        seeds = [seed0 + r for r in range(runs)]
+        recs = (run_replicas(cfg, seeds) if cfg.pop_size <= REPLICA_MAX_POP
+                else [run_ga(cfg, seed=x) for x in seeds])
         row = {"muL": float(mu), "runs": runs}
         for name, vals in (("discovery", [r.discovery for r in recs]), ("adaptation", [r.adaptation for r in recs])):
             ok = [v for v in vals if v is not None]

@@ -202,3 +202,38 @@ def test_jatam_fitness_matches_cpu():
             exp = d * d - int(np.count_nonzero((grid >= 0).reshape(d, d) != target))
         assert int(f[i]) == exp, (i, idx)
     ga.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,L,mode,mu,stop", [(512, 32, "asexual", 0.3, "adaptation"), (777, 24, "single_point", 1.0, "never"),
+                                               (4096, 64, "uniform", 0.1, "discovery"), (512, 32, "asexual", 4.0, "adaptation")])
+def test_replicas_equal_single_runs(n, L, mode, mu, stop):
+    """One replica launch == independent run_ga calls, record by record (trajectories, stop points)."""
+    cfg = E.GAConfig(pop_size=n, length=L, mu_L=mu, mode=mode, cutoff=600, target=min(25, L - 2), stop_when=stop)
+    seeds = [3, 17, 2205, 1 << 40]
+    reps = E.run_replicas(cfg, seeds)
+    for s, r in zip(seeds, reps):
+        x = E.run_ga(cfg, seed=s)
+        assert (r.generations, r.discovery, r.adaptation) == (x.generations, x.discovery, x.adaptation), s
+        assert np.array_equal(r.best, x.best) and np.array_equal(r.count_at_target, x.count_at_target)
+        assert np.allclose(r.mean, x.mean)
+
+
+@pytest.mark.gpu
+def test_replicas_final_population_and_init():
+    """Final populations and a non-zero initial population through the C ABI directly."""
+    from paper_2205_15311_b200 import _lib
+    n, L, R, gens = 300, 32, 5, 77
+    T = E.poisson_thresholds(0.5, L)
+    init = np.random.default_rng(1).integers(0, 1 << 32, (R, n), dtype=np.uint64)
+    seeds = np.arange(R, dtype=np.uint64) + 9
+    done, disc, adap = (np.zeros(R, np.int64) for _ in range(3))
+    fin = np.zeros((R, n), np.uint64)
+    P = _lib.ptr
+    _lib.check(_lib.lib().tv_ga_replicas(n, L, 2, P(T), R, P(seeds), P(init), 5, gens, 30, n // 2, 0, P(done),
+                                         P(disc), P(adap), None, None, None, P(fin), None))
+    for r in range(R):
+        pop = init[r].copy()
+        k, *_ = O.ga_run(pop, L, 2, T, int(seeds[r]), 5, gens, 30, n // 2, 0)
+        assert k == done[r] == gens
+        assert np.array_equal(fin[r], pop), r
