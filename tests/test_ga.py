@@ -161,14 +161,16 @@ def test_device_ga_equals_restatement(n, L, mode, lam, stop):
 def test_fujiyama_regime_desk_scale():
     """SPEC ACCEPTANCE 4 (runs=25, pop=512, L=32, cutoff=20000)."""
     med = []
-    for mu in (0.03, 0.1, 0.3):
-        d = [E.run_ga(E.GAConfig(mu_L=mu, stop_when="discovery"), seed=r).discovery for r in range(25)]
+    for mu in (0.03, 0.1, 0.3):  # 25 runs per point in one replica launch (== run_ga per seed)
+        d = [r.discovery for r in E.run_replicas(E.GAConfig(mu_L=mu, stop_when="discovery"), range(25))]
         d = [x if x is not None else 20000 for x in d]
         med.append(np.median(d))
     assert med[0] > med[1] > med[2], med
-    ok03 = sum(E.run_ga(E.GAConfig(mu_L=0.3), seed=100 + r).adaptation is not None for r in range(25))
-    cens4 = sum(E.run_ga(E.GAConfig(mu_L=4.0), seed=200 + r).adaptation is None for r in range(25))
+    ok03 = sum(r.adaptation is not None for r in E.run_replicas(E.GAConfig(mu_L=0.3), range(100, 125)))
+    cens4 = sum(r.adaptation is None for r in E.run_replicas(E.GAConfig(mu_L=4.0), range(200, 225)))
     assert ok03 >= 20 and cens4 >= 20, (ok03, cens4)
+    rows = E.sweep([0.1, 0.3], runs=25)  # SPEC:452 sweep rows through the device sweep
+    assert [r["muL"] for r in rows] == [0.1, 0.3] and rows[1]["adaptation"]["median"] is not None
 
 
 @pytest.mark.gpu
