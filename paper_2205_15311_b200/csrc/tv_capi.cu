@@ -1,5 +1,7 @@
 // tv_capi.cu -- extern "C" boundary of libtilevolve_b200.so (include/tilevolve_b200.h).
+#include <cub/device/device_partition.cuh>
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -222,21 +224,41 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
       // off for a = 3, where the 12-candidate proof costs more than it saves (S32
       // 2^24 block: 42.7 -> 45.5 ms).  TV_EARLY_UNBOUND=0/1 forces it off/on.
       const char *eu = getenv("TV_EARLY_UNBOUND");
+      const char *eo = getenv("TV_LONGEST_FIRST");
       P.tf_flags = nullptr;
+      P.order = nullptr;
       // (payload and fitness modes stop at the first UNBOUND run anyway)
-      if (!P.pay_mode && !P.fit_mode && (eu ? atoi(eu) != 0 : P.a <= 2)) {
-        uint32_t *flags;
+      const bool want_flags = !P.pay_mode && !P.fit_mode && (eu ? atoi(eu) != 0 : P.a <= 2);
+      // longest-first work order (histogram mode; classify mode keeps item order for its rows):
+      // full S_{2,8} 39.3 -> 38.5 ms, S32 2^24 block 43.1 -> 41.3 ms (the kernel tail shrinks).
+      // TV_LONGEST_FIRST=0 disables it.
+      const bool want_order = P.hist_mode && P.n <= 0xFFFFFFFFll && (eo ? atoi(eo) != 0 : true);
+      if (want_flags || want_order) {
+        uint32_t *flags = nullptr, *order = nullptr;
+        uint8_t *longrun = nullptr;
         const int64_t nw = (P.n + 31) / 32;
-        CK(S.get(&flags, (size_t)nw));
+        if (want_flags) CK(S.get(&flags, (size_t)nw));
+        if (want_order) { CK(S.get(&order, (size_t)P.n)); CK(S.get(&longrun, (size_t)P.n)); }
         const void *ff = P.strict
-            ? (P.a == 1 ? (const void *)k_trivial_flags<1, true>
-               : P.a == 2 ? (const void *)k_trivial_flags<2, true> : (const void *)k_trivial_flags<3, true>)
-            : (P.a == 1 ? (const void *)k_trivial_flags<1, false>
-               : P.a == 2 ? (const void *)k_trivial_flags<2, false> : (const void *)k_trivial_flags<3, false>);
+            ? (P.a == 1 ? (const void *)k_prepass<1, true>
+               : P.a == 2 ? (const void *)k_prepass<2, true> : (const void *)k_prepass<3, true>)
+            : (P.a == 1 ? (const void *)k_prepass<1, false>
+               : P.a == 2 ? (const void *)k_prepass<2, false> : (const void *)k_prepass<3, false>);
         const int64_t fb = std::min<int64_t>((nw * 32 + 255) / 256, (int64_t)nsm * 8);
-        void *fargs[] = {&P, &flags};
+        void *fargs[] = {&P, &flags, &longrun};
         CK(cudaLaunchKernel(ff, dim3((unsigned)fb), dim3(256), fargs, 0, st));
+        if (want_order) {  // long items first (index order), the rest after (reverse index order)
+          cub::CountingInputIterator<uint32_t> it(0);
+          unsigned long long *nsel;
+          CK(S.get(&nsel, 1));
+          size_t tmp_bytes = 0;
+          CK(cub::DevicePartition::Flagged(nullptr, tmp_bytes, it, longrun, order, nsel, P.n, st));
+          uint8_t *tmp;
+          CK(S.get(&tmp, tmp_bytes));
+          CK(cub::DevicePartition::Flagged(tmp, tmp_bytes, it, longrun, order, nsel, P.n, st));
+        }
         P.tf_flags = flags;
+        P.order = order;
       }
       void *args[] = {&P};
       CK(cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(threads), args, smem, st));
@@ -806,6 +828,7 @@ int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ga_run, 1024, h->smem));
   if (per_sm < 1) { delete h; return fail(TV_ERR_CUDA, "GA kernel does not fit one CTA per SM"); }
   h->nblocks = nsm;
+  if (const char *ec = getenv("TV_GA_CTAS")) h->nblocks = std::max(1, std::min(nsm, atoi(ec)));  // A/B only
   P.chunk = (n + h->nblocks - 1) / h->nblocks;
   h->device = dev;
   h->cur = 0;

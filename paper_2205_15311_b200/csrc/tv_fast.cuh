@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(TV_FAST_MAXT, TV_FAST_MINB) k_classify_fast(co
   int trivial_at = -1, first_unbound = -1, first_mismatch = -1;
   uint32_t hash0 = 0, best = 0, fit0 = 0;
   int64_t pslot = -1;  // histogram slot whose payload the claiming genome's replay writes
-  bool tfree = false;  // no run of this genome can go TRIVIAL (k_trivial_flags)
+  bool tfree = false;  // no run of this genome can go TRIVIAL (k_prepass)
   Cand<A, STRICT> K;
 
   for (;;) {
@@ -490,12 +490,13 @@ __global__ void __launch_bounds__(TV_FAST_MAXT, TV_FAST_MINB) k_classify_fast(co
           if (item >= P.n) {
             st = ST_DONE;
           } else {
-            idx = item_index(P.indices, P.start, P.chunk, P.stride, item);
+            const int64_t it = P.order ? (int64_t)P.order[item] : item;  // longest-first (k_prepass)
+            idx = item_index(P.indices, P.start, P.chunk, P.stride, it);
             uint32_t lab[12];  // decode labels (_k:384-401)
 #pragma unroll
             for (int te = 0; te < 12; te++) lab[te] = te < NC ? decode_label(P.dec, te, idx) : 0u;
             K.build(lab, A);
-            tfree = P.tf_flags ? ((P.tf_flags[item >> 5] >> (item & 31)) & 1u) != 0u : false;
+            tfree = P.tf_flags ? ((P.tf_flags[it >> 5] >> (it & 31)) & 1u) != 0u : false;
             trivial_at = first_unbound = first_mismatch = -1;
             run = 0;
             replay = 0;
@@ -597,29 +598,47 @@ __global__ void __launch_bounds__(TV_FAST_MAXT, TV_FAST_MINB) k_classify_fast(co
   }
 }
 
-// Per-item trivial-freedom bits for the early unbound cut-off: bit (i & 31)
-// of flags[i >> 5] for work item i.  Full-SIMT pre-pass (every lane runs the
-// same straight-line proof), so the divergent fold in k_classify_fast only
-// reads one bit.
+// Pre-pass over the work items (full SIMT: every lane runs the same straight-line
+// code), two optional products:
+//  * flags: trivial-freedom bits for the early unbound cut-off, bit (i & 31) of
+//    flags[i >> 5] for work item i (CandSwar::trivial_free);
+//  * longrun: 1 for a genome with a tile that bonds a copy of itself through
+//    opposite faces -- it can grow a straight line (long UNBOUND runs: in S_{2,8}
+//    33 % of the genomes, 45 % of the pops, 98 % of the slowest 0.1 %).  A
+//    stable partition (cub::DevicePartition::Flagged) puts those items first, so
+//    the kernel's tail is made of short genomes, and keeps index order inside the
+//    parts so the lanes of a warp still hold similar genomes.  Results cannot
+//    depend on the order (per-genome substreams, commutative histogram updates).
 template <int A, bool STRICT>
-__global__ void __launch_bounds__(256) k_trivial_flags(const __grid_constant__ ClassifyParams P, uint32_t *flags) {
+__global__ void __launch_bounds__(256) k_prepass(const __grid_constant__ ClassifyParams P, uint32_t *flags,
+                                                 uint8_t *longrun_out) {
   constexpr int NC = 4 * A;
   const int64_t nw = (P.n + 31) >> 5;
+  const int lane = threadIdx.x & 31;
   for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~(int64_t)31; base < nw * 32;
        base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t item = base + (threadIdx.x & 31);
-    bool f = false;
-    if (item < P.n) {
+    const int64_t item = base + lane;
+    bool f = false, longrun = false;
+    const bool valid = item < P.n;
+    if (valid) {
       const uint64_t idx = item_index(P.indices, P.start, P.chunk, P.stride, item);
       uint32_t lab[12];
 #pragma unroll
       for (int te = 0; te < 12; te++) lab[te] = te < NC ? decode_label(P.dec, te, idx) : 0u;
-      Cand<A, STRICT> K;
-      K.build_faces(lab);  // tiles >= A have all-zero faces: they never bond, so never pair
-      f = K.trivial_free();
+#pragma unroll
+      for (int t = 0; t < A; t++)  // N bonds S or E bonds W of the same tile (_k:90-93)
+        longrun |= bonds((int)lab[4 * t], (int)lab[4 * t + 2]) || bonds((int)lab[4 * t + 1], (int)lab[4 * t + 3]);
+      if (flags) {
+        Cand<A, STRICT> K;
+        K.build_faces(lab);  // tiles >= A have all-zero faces: they never bond, so never pair
+        f = K.trivial_free();
+      }
     }
-    const uint32_t w = __ballot_sync(0xFFFFFFFFu, f);
-    if ((threadIdx.x & 31) == 0) flags[base >> 5] = w;
+    if (flags) {
+      const uint32_t w = __ballot_sync(0xFFFFFFFFu, f);
+      if (lane == 0) flags[base >> 5] = w;
+    }
+    if (longrun_out && valid) longrun_out[item] = longrun ? 1 : 0;
   }
 }
 

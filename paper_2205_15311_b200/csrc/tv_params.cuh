@@ -48,6 +48,7 @@ struct ClassifyParams {
   int32_t cta_slots;        // fast kernel: per-CTA shared histogram slots (power of 2; 0 = off)
   int32_t service_thresh;   // fast kernel: parked lanes that trigger a warp service pass (0 = default)
   const uint32_t *tf_flags; // fast kernel: per-item trivial-freedom bits (early unbound cut-off), or nullptr
+  const uint32_t *order;    // fast kernel, histogram mode: work-item permutation (longest first), or nullptr
   unsigned long long *work; // dynamic work counter
   // generic kernel scratch (per thread, interleaved)
   int16_t *g_grid;
