@@ -1,7 +1,7 @@
 // tv_capi.cu -- extern "C" boundary of libtilevolve_b200.so (include/tilevolve_b200.h).
 #include <cub/device/device_partition.cuh>
 #include <cub/device/device_radix_sort.cuh>
-#include <cub/iterator/counting_input_iterator.cuh>
+#include <thrust/iterator/counting_iterator.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -248,7 +248,7 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
         void *fargs[] = {&P, &flags, &longrun};
         CK(cudaLaunchKernel(ff, dim3((unsigned)fb), dim3(256), fargs, 0, st));
         if (want_order) {  // long items first (index order), the rest after (reverse index order)
-          cub::CountingInputIterator<uint32_t> it(0);
+          thrust::counting_iterator<uint32_t> it(0);
           unsigned long long *nsel;
           CK(S.get(&nsel, 1));
           size_t tmp_bytes = 0;
