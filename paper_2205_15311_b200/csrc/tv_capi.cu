@@ -1,7 +1,5 @@
 // tv_capi.cu -- extern "C" boundary of libtilevolve_b200.so (include/tilevolve_b200.h).
-#include <cub/device/device_partition.cuh>
 #include <cub/device/device_radix_sort.cuh>
-#include <thrust/iterator/counting_iterator.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -224,45 +222,60 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
       // off for a = 3, where the 12-candidate proof costs more than it saves (S32
       // 2^24 block: 42.7 -> 45.5 ms).  TV_EARLY_UNBOUND=0/1 forces it off/on.
       const char *eu = getenv("TV_EARLY_UNBOUND");
-      const char *eo = getenv("TV_LONGEST_FIRST");
-      P.tf_flags = nullptr;
-      P.order = nullptr;
+      const char *eo = getenv("TV_ORDER");
       // (payload and fitness modes stop at the first UNBOUND run anyway)
       const bool want_flags = !P.pay_mode && !P.fit_mode && (eu ? atoi(eu) != 0 : P.a <= 2);
-      // longest-first work order (histogram mode; classify mode keeps item order for its rows):
-      // full S_{2,8} 39.3 -> 38.5 ms, S32 2^24 block 43.1 -> 41.3 ms (the kernel tail shrinks).
-      // TV_LONGEST_FIRST=0 disables it.
-      const bool want_order = P.hist_mode && P.n <= 0xFFFFFFFFll && (eo ? atoi(eo) != 0 : true);
-      if (want_flags || want_order) {
-        uint32_t *flags = nullptr, *order = nullptr;
-        uint8_t *longrun = nullptr;
-        const int64_t nw = (P.n + 31) / 32;
-        if (want_flags) CK(S.get(&flags, (size_t)nw));
-        if (want_order) { CK(S.get(&order, (size_t)P.n)); CK(S.get(&longrun, (size_t)P.n)); }
-        const void *ff = P.strict
-            ? (P.a == 1 ? (const void *)k_prepass<1, true>
-               : P.a == 2 ? (const void *)k_prepass<2, true> : (const void *)k_prepass<3, true>)
-            : (P.a == 1 ? (const void *)k_prepass<1, false>
-               : P.a == 2 ? (const void *)k_prepass<2, false> : (const void *)k_prepass<3, false>);
-        const int64_t fb = std::min<int64_t>((nw * 32 + 255) / 256, (int64_t)nsm * 8);
-        void *fargs[] = {&P, &flags, &longrun};
-        CK(cudaLaunchKernel(ff, dim3((unsigned)fb), dim3(256), fargs, 0, st));
-        if (want_order) {  // long items first (index order), the rest after (reverse index order)
-          thrust::counting_iterator<uint32_t> it(0);
-          unsigned long long *nsel;
-          CK(S.get(&nsel, 1));
-          size_t tmp_bytes = 0;
-          CK(cub::DevicePartition::Flagged(nullptr, tmp_bytes, it, longrun, order, nsel, P.n, st));
-          uint8_t *tmp;
-          CK(S.get(&tmp, tmp_bytes));
-          CK(cub::DevicePartition::Flagged(tmp, tmp_bytes, it, longrun, order, nsel, P.n, st));
-        }
-        P.tf_flags = flags;
-        P.order = order;
+      // behaviour-sorted work order (histogram mode; classify mode keeps item order for its
+      // rows): see k_prepass.  TV_ORDER=0 disables it.
+      const bool want_order = P.hist_mode && (eo ? atoi(eo) != 0 : true);
+      // histogram mode runs in slices of <= 2^26 items (sort and flag scratch stay bounded;
+      // the histogram accumulates across slices)
+      const int64_t n_all = P.n, slice = P.hist_mode ? ((int64_t)1 << 26) : n_all;
+      const int64_t smax = std::min(n_all, slice);
+      uint32_t *flags = nullptr, *order = nullptr, *iota = nullptr;
+      uint16_t *key = nullptr, *key_sorted = nullptr;
+      uint8_t *tmp = nullptr;
+      size_t tmp_bytes = 0;
+      const int64_t nwmax = (smax + 31) / 32;
+      if (want_flags) CK(S.get(&flags, (size_t)nwmax));
+      if (want_order) {
+        CK(S.get(&order, (size_t)smax)); CK(S.get(&iota, (size_t)smax));
+        CK(S.get(&key, (size_t)smax)); CK(S.get(&key_sorted, (size_t)smax));
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key, key_sorted, iota, order, (int)smax, 0, 9, st));
+        CK(S.get(&tmp, tmp_bytes));
       }
-      void *args[] = {&P};
-      CK(cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(threads), args, smem, st));
-      g_launch[0] = 1; g_launch[1] = blocks; g_launch[2] = threads; g_launch[3] = (int64_t)smem; g_launch[4] = 1;
+      const void *ff = P.strict
+          ? (P.a == 1 ? (const void *)k_prepass<1, true>
+             : P.a == 2 ? (const void *)k_prepass<2, true> : (const void *)k_prepass<3, true>)
+          : (P.a == 1 ? (const void *)k_prepass<1, false>
+             : P.a == 2 ? (const void *)k_prepass<2, false> : (const void *)k_prepass<3, false>);
+      for (int64_t off = 0; off < n_all; off += slice) {
+        P.item0 = off;
+        P.n = std::min(slice, n_all - off);
+        P.tf_flags = nullptr;
+        P.order = nullptr;
+        if (off > 0) CK(cudaMemsetAsync(work, 0, sizeof(unsigned long long), st));
+        if (want_flags || want_order) {
+          const int64_t nw = (P.n + 31) / 32;
+          const int64_t fb = std::min<int64_t>((nw * 32 + 255) / 256, (int64_t)nsm * 8);
+          uint16_t *kk = want_order ? key : nullptr;
+          uint32_t *ff_flags = want_flags ? flags : nullptr;
+          void *fargs[] = {&P, &ff_flags, &kk, &iota};
+          CK(cudaLaunchKernel(ff, dim3((unsigned)fb), dim3(256), fargs, 0, st));
+          if (want_order) {  // stable LSD radix sort of the items by their 9-bit behaviour key
+            size_t tb = tmp_bytes;
+            CK(cub::DeviceRadixSort::SortPairs(tmp, tb, key, key_sorted, iota, order, (int)P.n, 0, 9, st));
+          }
+          P.tf_flags = ff_flags;
+          P.order = want_order ? order : nullptr;
+        }
+        void *args[] = {&P};
+        CK(cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(threads), args, smem, st));
+      }
+      P.n = n_all;
+      P.item0 = 0;
+      g_launch[0] = 1; g_launch[1] = blocks; g_launch[2] = threads; g_launch[3] = (int64_t)smem;
+      g_launch[4] = (n_all + slice - 1) / slice;
       return 0;
     }
   }

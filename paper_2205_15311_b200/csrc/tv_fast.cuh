@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(TV_FAST_MAXT, TV_FAST_MINB) k_classify_fast(co
             st = ST_DONE;
           } else {
             const int64_t it = P.order ? (int64_t)P.order[item] : item;  // longest-first (k_prepass)
-            idx = item_index(P.indices, P.start, P.chunk, P.stride, it);
+            idx = item_index(P.indices, P.start, P.chunk, P.stride, P.item0 + it);
             uint32_t lab[12];  // decode labels (_k:384-401)
 #pragma unroll
             for (int te = 0; te < 12; te++) lab[te] = te < NC ? decode_label(P.dec, te, idx) : 0u;
@@ -602,32 +602,59 @@ __global__ void __launch_bounds__(TV_FAST_MAXT, TV_FAST_MINB) k_classify_fast(co
 // code), two optional products:
 //  * flags: trivial-freedom bits for the early unbound cut-off, bit (i & 31) of
 //    flags[i >> 5] for work item i (CandSwar::trivial_free);
-//  * longrun: 1 for a genome with a tile that bonds a copy of itself through
-//    opposite faces -- it can grow a straight line (long UNBOUND runs: in S_{2,8}
-//    33 % of the genomes, 45 % of the pops, 98 % of the slowest 0.1 %).  A
-//    stable partition (cub::DevicePartition::Flagged) puts those items first, so
-//    the kernel's tail is made of short genomes, and keeps index order inside the
-//    parts so the lanes of a warp still hold similar genomes.  Results cannot
-//    depend on the order (per-genome substreams, commutative histogram updates).
+//  * key: a 9-bit behaviour key per genome for histogram mode; items are stably
+//    radix-sorted by it, so (1) line-prone genomes (a tile bonds a copy of itself
+//    through opposite faces: long UNBOUND runs -- in S_{2,8} 33 % of the genomes,
+//    45 % of the pops, 98 % of the slowest 0.1 %) run first and the kernel's tail
+//    is made of short genomes, and (2) the lanes of a warp hold genomes of the same
+//    structure (seed self-bonding, bondable faces of the seed and of the other
+//    tiles), whose runs have similar lengths and outcomes: fewer idle lanes.
+//    Results cannot depend on the order (per-genome substreams, commutative
+//    histogram updates).
 template <int A, bool STRICT>
 __global__ void __launch_bounds__(256) k_prepass(const __grid_constant__ ClassifyParams P, uint32_t *flags,
-                                                 uint8_t *longrun_out) {
+                                                 uint16_t *key_out, uint32_t *iota_out) {
   constexpr int NC = 4 * A;
   const int64_t nw = (P.n + 31) >> 5;
   const int lane = threadIdx.x & 31;
   for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~(int64_t)31; base < nw * 32;
        base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t item = base + lane;
-    bool f = false, longrun = false;
+    bool f = false;
     const bool valid = item < P.n;
     if (valid) {
-      const uint64_t idx = item_index(P.indices, P.start, P.chunk, P.stride, item);
+      const uint64_t idx = item_index(P.indices, P.start, P.chunk, P.stride, P.item0 + item);
       uint32_t lab[12];
 #pragma unroll
       for (int te = 0; te < 12; te++) lab[te] = te < NC ? decode_label(P.dec, te, idx) : 0u;
+      if (key_out) {
+        // behaviour key (bonds, _k:90-93): line-prone (a tile bonds a copy of itself through
+        // opposite faces), seed tile bonds itself, bondable faces of the seed / other tiles
+        uint32_t present = 0;
 #pragma unroll
-      for (int t = 0; t < A; t++)  // N bonds S or E bonds W of the same tile (_k:90-93)
-        longrun |= bonds((int)lab[4 * t], (int)lab[4 * t + 2]) || bonds((int)lab[4 * t + 1], (int)lab[4 * t + 3]);
+        for (int te = 0; te < NC; te++) present |= 1u << lab[te];
+        bool line = false, self0 = false;
+        int nb0 = 0, nbr = 0;
+#pragma unroll
+        for (int t = 0; t < A; t++)
+          line |= bonds((int)lab[4 * t], (int)lab[4 * t + 2]) || bonds((int)lab[4 * t + 1], (int)lab[4 * t + 3]);
+#pragma unroll
+        for (int te = 0; te < NC; te++) {
+          const uint32_t x = lab[te];
+          const uint32_t px = x ? (((x - 1u) ^ 1u) + 1u) : 31u;  // partner; label 0 bonds nothing
+          const bool can = px < 31u && ((present >> px) & 1u);
+          if (te < 4) {
+            nb0 += can;
+#pragma unroll
+            for (int g = 0; g < 4; g++) self0 |= bonds((int)x, (int)lab[g]);
+          } else {
+            nbr += can;
+          }
+        }
+        key_out[item] = (uint16_t)(((line ? 0u : 1u) << 8) | ((self0 ? 0u : 1u) << 7) |
+                                   ((uint32_t)(4 - nb0) << 4) | (uint32_t)(8 - nbr));
+        iota_out[item] = (uint32_t)item;
+      }
       if (flags) {
         Cand<A, STRICT> K;
         K.build_faces(lab);  // tiles >= A have all-zero faces: they never bond, so never pair
@@ -638,7 +665,6 @@ __global__ void __launch_bounds__(256) k_prepass(const __grid_constant__ Classif
       const uint32_t w = __ballot_sync(0xFFFFFFFFu, f);
       if (lane == 0) flags[base >> 5] = w;
     }
-    if (longrun_out && valid) longrun_out[item] = longrun ? 1 : 0;
   }
 }
 

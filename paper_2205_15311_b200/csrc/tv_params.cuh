@@ -14,6 +14,7 @@ struct ClassifyParams {
   uint64_t start;           // range mode: item i -> index start + (i / chunk) * stride + (i % chunk)
   uint64_t chunk, stride;   // chunk == 0: plain range start + i
   int64_t n;                // work items
+  int64_t item0;            // histogram-mode slice: work item i of this launch is item item0 + i
   int32_t a, d, strict, q, kmax, hist_k;
   int32_t ks[kMaxKs];       // ascending prefix redundancies (_k:410-413)
   uint64_t seed;
@@ -48,7 +49,7 @@ struct ClassifyParams {
   int32_t cta_slots;        // fast kernel: per-CTA shared histogram slots (power of 2; 0 = off)
   int32_t service_thresh;   // fast kernel: parked lanes that trigger a warp service pass (0 = default)
   const uint32_t *tf_flags; // fast kernel: per-item trivial-freedom bits (early unbound cut-off), or nullptr
-  const uint32_t *order;    // fast kernel, histogram mode: work-item permutation (longest first), or nullptr
+  const uint32_t *order;    // fast kernel, histogram mode: work-item permutation (k_prepass sort), or nullptr
   unsigned long long *work; // dynamic work counter
   // generic kernel scratch (per thread, interleaved)
   int16_t *g_grid;
