@@ -182,9 +182,9 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
     const char *es = getenv("TV_STACK_S"), *ec = getenv("TV_CTA_SLOTS"), *et = getenv("TV_SERVICE_THRESH");
     const char *eth = getenv("TV_FAST_THREADS");
     P.service_thresh = et ? atoi(et) : 0;
-    // per-CTA phenotype cache: 256 slots for a = 3 (S32: ~5e5 phenotypes; 2^24 block 43.6 -> 42.4 ms),
-    // 128 otherwise (S28: 2,233 phenotypes; 256 measured neutral, 512 halves occupancy)
-    P.cta_slots = P.hist_mode ? (ec ? atoi(ec) : (P.a >= 3 ? 256 : 128)) : 0;
+    // per-CTA phenotype cache: 256 slots (with the behaviour-sorted order a CTA sees many
+    // phenotypes of alike genomes: S28 32.3 -> 31.6 ms vs 128 slots; 512 halves occupancy)
+    P.cta_slots = P.hist_mode ? (ec ? atoi(ec) : 256) : 0;
     int threads = eth ? std::min(atoi(eth), TV_FAST_MAXT) & ~31 : TV_FAST_MAXT;
     if (es) {
       P.S = std::max(4, atoi(es)) & ~1;
@@ -241,7 +241,7 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
       if (want_order) {
         CK(S.get(&order, (size_t)smax)); CK(S.get(&iota, (size_t)smax));
         CK(S.get(&key, (size_t)smax)); CK(S.get(&key_sorted, (size_t)smax));
-        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key, key_sorted, iota, order, (int)smax, 0, 9, st));
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key, key_sorted, iota, order, (int)smax, 0, 10, st));
         CK(S.get(&tmp, tmp_bytes));
       }
       const void *ff = P.strict
@@ -262,9 +262,9 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
           uint32_t *ff_flags = want_flags ? flags : nullptr;
           void *fargs[] = {&P, &ff_flags, &kk, &iota};
           CK(cudaLaunchKernel(ff, dim3((unsigned)fb), dim3(256), fargs, 0, st));
-          if (want_order) {  // stable LSD radix sort of the items by their 9-bit behaviour key
+          if (want_order) {  // stable LSD radix sort of the items by their 10-bit behaviour key
             size_t tb = tmp_bytes;
-            CK(cub::DeviceRadixSort::SortPairs(tmp, tb, key, key_sorted, iota, order, (int)P.n, 0, 9, st));
+            CK(cub::DeviceRadixSort::SortPairs(tmp, tb, key, key_sorted, iota, order, (int)P.n, 0, 10, st));
           }
           P.tf_flags = ff_flags;
           P.order = want_order ? order : nullptr;

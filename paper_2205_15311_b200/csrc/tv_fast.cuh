@@ -602,13 +602,14 @@ __global__ void __launch_bounds__(TV_FAST_MAXT, TV_FAST_MINB) k_classify_fast(co
 // code), two optional products:
 //  * flags: trivial-freedom bits for the early unbound cut-off, bit (i & 31) of
 //    flags[i >> 5] for work item i (CandSwar::trivial_free);
-//  * key: a 9-bit behaviour key per genome for histogram mode; items are stably
+//  * key: a 10-bit behaviour key per genome for histogram mode; items are stably
 //    radix-sorted by it, so (1) line-prone genomes (a tile bonds a copy of itself
 //    through opposite faces: long UNBOUND runs -- in S_{2,8} 33 % of the genomes,
 //    45 % of the pops, 98 % of the slowest 0.1 %) run first and the kernel's tail
 //    is made of short genomes, and (2) the lanes of a warp hold genomes of the same
-//    structure (seed self-bonding, bondable faces of the seed and of the other
-//    tiles), whose runs have similar lengths and outcomes: fewer idle lanes.
+//    structure (seed self-bonding, bondable faces of the seed, other tiles
+//    self-bonding, their bondable faces), whose runs have similar lengths and
+//    outcomes: fewer idle lanes.
 //    Results cannot depend on the order (per-genome substreams, commutative
 //    histogram updates).
 template <int A, bool STRICT>
@@ -633,7 +634,7 @@ __global__ void __launch_bounds__(256) k_prepass(const __grid_constant__ Classif
         uint32_t present = 0;
 #pragma unroll
         for (int te = 0; te < NC; te++) present |= 1u << lab[te];
-        bool line = false, self0 = false;
+        bool line = false, self0 = false, selfr = false;
         int nb0 = 0, nbr = 0;
 #pragma unroll
         for (int t = 0; t < A; t++)
@@ -649,10 +650,12 @@ __global__ void __launch_bounds__(256) k_prepass(const __grid_constant__ Classif
             for (int g = 0; g < 4; g++) self0 |= bonds((int)x, (int)lab[g]);
           } else {
             nbr += can;
+#pragma unroll
+            for (int g = 4; g < NC; g++) selfr |= (g >> 2) == (te >> 2) && bonds((int)x, (int)lab[g]);
           }
         }
-        key_out[item] = (uint16_t)(((line ? 0u : 1u) << 8) | ((self0 ? 0u : 1u) << 7) |
-                                   ((uint32_t)(4 - nb0) << 4) | (uint32_t)(8 - nbr));
+        key_out[item] = (uint16_t)(((line ? 0u : 1u) << 9) | ((self0 ? 0u : 1u) << 8) |
+                                   ((uint32_t)(4 - nb0) << 5) | ((selfr ? 0u : 1u) << 4) | (uint32_t)(8 - nbr));
         iota_out[item] = (uint32_t)item;
       }
       if (flags) {
