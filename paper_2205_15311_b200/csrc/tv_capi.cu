@@ -225,9 +225,11 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
       const char *eo = getenv("TV_ORDER");
       // (payload and fitness modes stop at the first UNBOUND run anyway)
       const bool want_flags = !P.pay_mode && !P.fit_mode && (eu ? atoi(eu) != 0 : P.a <= 2);
-      // behaviour-sorted work order (histogram mode; classify mode keeps item order for its
-      // rows): see k_prepass.  TV_ORDER=0 disables it.
-      const bool want_order = P.hist_mode && (eo ? atoi(eo) != 0 : true);
+      // behaviour-sorted processing order for every mode (outputs stay addressed by item):
+      // see k_prepass.  Classify-type calls above 2^30 items keep item order (sort scratch).
+      // TV_ORDER=0 disables it.
+      const bool want_order = (P.hist_mode || P.n <= ((int64_t)1 << 30)) && P.n >= 4096 &&
+                              (eo ? atoi(eo) != 0 : true);
       // histogram mode runs in slices of <= 2^26 items (sort and flag scratch stay bounded;
       // the histogram accumulates across slices)
       const int64_t n_all = P.n, slice = P.hist_mode ? ((int64_t)1 << 26) : n_all;

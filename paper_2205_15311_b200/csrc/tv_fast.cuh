@@ -490,13 +490,15 @@ __global__ void __launch_bounds__(TV_FAST_MAXT, TV_FAST_MINB) k_classify_fast(co
           if (item >= P.n) {
             st = ST_DONE;
           } else {
-            const int64_t it = P.order ? (int64_t)P.order[item] : item;  // longest-first (k_prepass)
-            idx = item_index(P.indices, P.start, P.chunk, P.stride, P.item0 + it);
+            // behaviour-sorted processing order (k_prepass); every per-item output and flag below
+            // is addressed by the item's own number, so the order is invisible to the caller
+            if (P.order) item = (int64_t)P.order[item];
+            idx = item_index(P.indices, P.start, P.chunk, P.stride, P.item0 + item);
             uint32_t lab[12];  // decode labels (_k:384-401)
 #pragma unroll
             for (int te = 0; te < 12; te++) lab[te] = te < NC ? decode_label(P.dec, te, idx) : 0u;
             K.build(lab, A);
-            tfree = P.tf_flags ? ((P.tf_flags[it >> 5] >> (it & 31)) & 1u) != 0u : false;
+            tfree = P.tf_flags ? ((P.tf_flags[item >> 5] >> (item & 31)) & 1u) != 0u : false;
             trivial_at = first_unbound = first_mismatch = -1;
             run = 0;
             replay = 0;
@@ -602,7 +604,7 @@ __global__ void __launch_bounds__(TV_FAST_MAXT, TV_FAST_MINB) k_classify_fast(co
 // code), two optional products:
 //  * flags: trivial-freedom bits for the early unbound cut-off, bit (i & 31) of
 //    flags[i >> 5] for work item i (CandSwar::trivial_free);
-//  * key: a 10-bit behaviour key per genome for histogram mode; items are stably
+//  * key: a 10-bit behaviour key per genome; the items are stably
 //    radix-sorted by it, so (1) line-prone genomes (a tile bonds a copy of itself
 //    through opposite faces: long UNBOUND runs -- in S_{2,8} 33 % of the genomes,
 //    45 % of the pops, 98 % of the slowest 0.1 %) run first and the kernel's tail
