@@ -243,7 +243,7 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
       if (want_order) {
         CK(S.get(&order, (size_t)smax)); CK(S.get(&iota, (size_t)smax));
         CK(S.get(&key, (size_t)smax)); CK(S.get(&key_sorted, (size_t)smax));
-        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key, key_sorted, iota, order, (int)smax, 0, 10, st));
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key, key_sorted, iota, order, (int)smax, 0, TV_KEY_BITS, st));
         CK(S.get(&tmp, tmp_bytes));
       }
       const void *ff = P.strict
@@ -266,7 +266,7 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
           CK(cudaLaunchKernel(ff, dim3((unsigned)fb), dim3(256), fargs, 0, st));
           if (want_order) {  // stable LSD radix sort of the items by their 10-bit behaviour key
             size_t tb = tmp_bytes;
-            CK(cub::DeviceRadixSort::SortPairs(tmp, tb, key, key_sorted, iota, order, (int)P.n, 0, 10, st));
+            CK(cub::DeviceRadixSort::SortPairs(tmp, tb, key, key_sorted, iota, order, (int)P.n, 0, TV_KEY_BITS, st));
           }
           P.tf_flags = ff_flags;
           P.order = want_order ? order : nullptr;

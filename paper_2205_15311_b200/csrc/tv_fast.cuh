@@ -228,6 +228,11 @@ template <bool S> struct Cand<1, S> : CandSwar<uint32_t, 8, S> {};
 
 enum { ST_NEED = 0, ST_RUN = 1, ST_DONE = 2 };
 
+#ifndef TV_KEY_TF
+#define TV_KEY_TF 2  // trivial-freedom as the lowest key bit (S28 31.4 -> 31.0 ms; 1 = top bit, 0 = off)
+#endif
+#define TV_KEY_BITS (TV_KEY_TF ? 11 : 10)  // width of the k_prepass behaviour key
+
 #ifndef TV_FAST_MINB
 #define TV_FAST_MINB 2
 #endif
@@ -630,9 +635,15 @@ __global__ void __launch_bounds__(256) k_prepass(const __grid_constant__ Classif
       uint32_t lab[12];
 #pragma unroll
       for (int te = 0; te < 12; te++) lab[te] = te < NC ? decode_label(P.dec, te, idx) : 0u;
+      if (flags) {
+        Cand<A, STRICT> K;
+        K.build_faces(lab);  // tiles >= A have all-zero faces: they never bond, so never pair
+        f = K.trivial_free();
+      }
       if (key_out) {
         // behaviour key (bonds, _k:90-93): line-prone (a tile bonds a copy of itself through
-        // opposite faces), seed tile bonds itself, bondable faces of the seed / other tiles
+        // opposite faces), seed tile bonds itself, bondable faces of the seed, another tile
+        // bonds itself, bondable faces of the other tiles; smaller keys run first
         uint32_t present = 0;
 #pragma unroll
         for (int te = 0; te < NC; te++) present |= 1u << lab[te];
@@ -656,14 +667,15 @@ __global__ void __launch_bounds__(256) k_prepass(const __grid_constant__ Classif
             for (int g = 4; g < NC; g++) selfr |= (g >> 2) == (te >> 2) && bonds((int)x, (int)lab[g]);
           }
         }
-        key_out[item] = (uint16_t)(((line ? 0u : 1u) << 9) | ((self0 ? 0u : 1u) << 8) |
-                                   ((uint32_t)(4 - nb0) << 5) | ((selfr ? 0u : 1u) << 4) | (uint32_t)(8 - nbr));
+#ifndef TV_KEY_TF
+#define TV_KEY_TF 2  // trivial-freedom as the lowest key bit (S28 31.4 -> 31.0 ms; 1 = top bit, 0 = off)
+#endif
+        uint32_t kk = ((line ? 0u : 1u) << 9) | ((self0 ? 0u : 1u) << 8) | ((uint32_t)(4 - nb0) << 5) |
+                      ((selfr ? 0u : 1u) << 4) | (uint32_t)(8 - nbr);
+        if (TV_KEY_TF == 1) kk |= (f ? 0u : 1u) << 10;
+        if (TV_KEY_TF == 2) kk = (kk << 1) | (f ? 0u : 1u);
+        key_out[item] = (uint16_t)kk;
         iota_out[item] = (uint32_t)item;
-      }
-      if (flags) {
-        Cand<A, STRICT> K;
-        K.build_faces(lab);  // tiles >= A have all-zero faces: they never bond, so never pair
-        f = K.trivial_free();
       }
     }
     if (flags) {
