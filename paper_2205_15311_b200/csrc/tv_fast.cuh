@@ -667,9 +667,6 @@ __global__ void __launch_bounds__(256) k_prepass(const __grid_constant__ Classif
             for (int g = 4; g < NC; g++) selfr |= (g >> 2) == (te >> 2) && bonds((int)x, (int)lab[g]);
           }
         }
-#ifndef TV_KEY_TF
-#define TV_KEY_TF 2  // trivial-freedom as the lowest key bit (S28 31.4 -> 31.0 ms; 1 = top bit, 0 = off)
-#endif
         uint32_t kk = ((line ? 0u : 1u) << 9) | ((self0 ? 0u : 1u) << 8) | ((uint32_t)(4 - nb0) << 5) |
                       ((selfr ? 0u : 1u) << 4) | (uint32_t)(8 - nbr);
         if (TV_KEY_TF == 1) kk |= (f ? 0u : 1u) << 10;
