@@ -5,8 +5,10 @@ ks=(1,2,4,8), hist_k=8, seed 0, strict contacts) into the device phenotype
 histogram: decode -> up to 8 movelist assemblies -> fold -> histogram insert,
 all in the sm_100a bitboard kernel.  With N ranks the index range is dealt out
 in round-robin chunks (strong scaling: the job is always the whole space) and
-the per-rank histograms are combined with one NCCL exchange
-(paper_2205_15311_b200.distributed.allreduce_histogram) inside the step.
+the per-rank histograms are combined with one device-resident NCCL exchange
+(paper_2205_15311_b200.distributed.allreduce_device_histogram: raw rows packed on
+the GPU, one all_gather + one all_reduce over NVLink, merge on the GPU, export)
+inside the step.
 
   value : device-timed (CUDA events, max over ranks) genomes/s, no host I/O.
   e2e   : the same job through the public API classify.enumerate_space (host
@@ -234,7 +236,7 @@ def s32_bench(args, rank: int, world: int, stream) -> dict:
     import torch.distributed as dist
     from paper_2205_15311_b200 import _lib
     from paper_2205_15311_b200.classify import DeviceHistogram, shape_words_for
-    from paper_2205_15311_b200.distributed import allreduce_histogram
+    from paper_2205_15311_b200.distributed import allreduce_device_histogram
     from paper_2205_15311_b200.genome import space_from_preset
 
     L = _lib.lib()
@@ -259,7 +261,7 @@ def s32_bench(args, rank: int, world: int, stream) -> dict:
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     run(mine * chunk)
-    merged = allreduce_histogram(hist.export(sp), None) if world > 1 else None
+    merged = allreduce_device_histogram(hist, None) if world > 1 else None
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
@@ -390,7 +392,7 @@ def main():
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
     from paper_2205_15311_b200 import _lib
     from paper_2205_15311_b200.classify import DeviceHistogram, enumerate_space, shape_words_for
-    from paper_2205_15311_b200.distributed import allreduce_histogram, enumerate_space_distributed
+    from paper_2205_15311_b200.distributed import allreduce_device_histogram, enumerate_space_distributed
 
     L = _lib.lib()
     space = s28_space()
@@ -422,7 +424,7 @@ def main():
     for _ in range(args.warmup):
         enumerate_step()
         if world > 1:
-            allreduce_histogram(hist.export(sp), None)
+            allreduce_device_histogram(hist, None)
     barrier()
     # ---- timed region: K steps, L2 flushed between steps (outside the events)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
@@ -438,8 +440,7 @@ def main():
             _lib.check(L.tv_enumerate_chunks(rank * CHUNK, count, CHUNK, CHUNK * world, a, bpl, _lib.ptr(mp),
                                              _lib.ptr(mv), mp.shape[0], _lib.ptr(fp), fp.shape[0], 19, _lib.ptr(ks),
                                              ks.shape[0], 8, 0, 1, hist._h, sp))
-            if world > 1:
-                allreduce_histogram(hist.export(sp), None)
+            merged = allreduce_device_histogram(hist, None) if world > 1 else None
             e2.record(stream)
         barrier()
     info = _lib.launch_info()
@@ -454,7 +455,7 @@ def main():
     value = N_S28 / (ms_per_step / 1e3)
 
     # correctness of what was timed: the exported histogram equals the reference aggregate
-    final = hist.export(sp) if world == 1 else allreduce_histogram(hist.export(sp), None)
+    final = hist.export(sp) if world == 1 else merged
     tallies_ok = final.tallies.tolist() == [[7448198, 5894957, 0, 3434061, 0], [6939346, 6865723, 214055, 2758092, 0],
                                             [6697803, 7791627, 223880, 2063906, 0], [6631160, 8336639, 199388, 1610029, 0]]
 

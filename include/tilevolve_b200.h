@@ -122,6 +122,16 @@ int tv_hist_export(tv_hist *h, int64_t max_records, uint32_t *keys, uint64_t *de
                    uint64_t *shape, int64_t *tallies, int64_t *n_out, void *stream);
 /* Merge records (same layout as export, [h|d]) and tallies (host, may be NULL)
  * into h: counts add, representatives take the minimum. */
+/* Multi-GPU exchange (device-resident, no payload fix-up on the way): pack the raw
+ * records as rows {key, det, steric, rep_det, rep_any, pay_idx, whc, shape[W]}
+ * (7 + W u64 each; pay_idx = the genome whose payload the row carries) and the
+ * tallies [q x 5]; rows/tallies [h|d].  replace_rows clears the histogram (keeping
+ * its enumeration parameters) and merges the rows of all ranks: counts added,
+ * representatives lowered, payload = the lowest payload owner; tv_hist_export then
+ * re-derives the payloads whose owner is not the representative. */
+int tv_hist_pack(tv_hist *h, int64_t max_records, uint64_t *rows, int64_t *tallies, int64_t *n_out,
+                 void *stream);
+int tv_hist_replace_rows(tv_hist *h, int64_t n, const uint64_t *rows, const int64_t *tallies, void *stream);
 int tv_hist_merge(tv_hist *h, int64_t n, const uint32_t *keys, const uint64_t *det, const uint64_t *steric,
                   const uint64_t *rep_det, const uint64_t *rep_any, const uint8_t *w, const uint8_t *hh,
                   const uint16_t *cells, const uint64_t *shape, const int64_t *tallies, void *stream);

@@ -58,6 +58,8 @@ _SIGS = {
     "tv_hist_clear": (_i32, [_p, _p]),
     "tv_hist_count": (_i32, [_p, _p, _p, _p]),
     "tv_hist_export": (_i32, [_p, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "tv_hist_pack": (_i32, [_p, _i64, _p, _p, _p, _p]),
+    "tv_hist_replace_rows": (_i32, [_p, _i64, _p, _p, _p]),
     "tv_hist_merge": (_i32, [_p, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "tv_enumerate_range": (_i32, [_u64, _u64, _i32, _i32, _p, _p, _i64, _p, _i64, _i32, _p, _i64, _i32, _u64, _i32,
                                   _p, _p]),

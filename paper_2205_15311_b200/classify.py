@@ -472,6 +472,24 @@ class DeviceHistogram:
                                              P(out.tallies), ctypes.byref(got), stream))
         return out
 
+    @property
+    def row_width(self) -> int:
+        return 7 + self.W
+
+    def pack_into(self, rows, tallies, stream=None) -> int:
+        """Raw records into ``rows`` (torch int64 [>= n, 7 + W], device or host) and the
+        tallies into ``tallies`` ([q, 5] int64); returns n (tv_hist_pack)."""
+        n = ctypes.c_int64()
+        _lib.check(_lib.lib().tv_hist_pack(self._h, int(rows.shape[0]), _lib.ptr(rows), _lib.ptr(tallies),
+                                           ctypes.byref(n), stream or _lib.stream_of(rows)))
+        return n.value
+
+    def replace_rows(self, rows, tallies, stream=None) -> None:
+        """Clear and merge packed rows of several histograms (tv_hist_replace_rows); rows whose
+        first word is 0 are padding."""
+        _lib.check(_lib.lib().tv_hist_replace_rows(self._h, int(rows.shape[0]), _lib.ptr(rows), _lib.ptr(tallies),
+                                                   stream or _lib.stream_of(rows)))
+
     def merge(self, hist: Histogram, stream=None) -> None:
         P = _lib.ptr
         tal = np.ascontiguousarray(hist.tallies, np.int64)

@@ -691,6 +691,84 @@ int tv_hist_export(tv_hist *h, int64_t max_records, uint32_t *keys, uint64_t *de
   return 0;
 }
 
+int tv_hist_pack(tv_hist *h, int64_t max_records, uint64_t *rows, int64_t *tallies, int64_t *n_out,
+                 void *stream) {
+  if (!h) return fail(TV_ERR_ARG, "null histogram");
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t n = 0;
+  int32_t ovf = 0;
+  if (int rc = tv_hist_count(h, &n, &ovf, stream)) return rc;
+  if (ovf) return fail(TV_ERR_HIST_FULL, "histogram overflowed its %lld slots", (long long)h->H.cap);
+  if (n > max_records) return fail(TV_ERR_ARG, "%lld records do not fit max_records=%lld", (long long)n, (long long)max_records);
+  const HistDev &H = h->H;
+  bool any_host = false;
+  {
+    Scratch S(st);
+    uint32_t *keys, *slots;
+    unsigned int *cnt;
+    CK(S.get(&keys, std::max<int64_t>(n, 1))); CK(S.get(&slots, std::max<int64_t>(n, 1))); CK(S.get(&cnt, 1));
+    CK(cudaMemsetAsync(cnt, 0, 4, st));
+    k_hist_compact<<<256, 256, 0, st>>>(H, keys, slots, cnt);
+    CK(cudaGetLastError());
+    unsigned long long *d_rows;
+    bool hr;
+    if (int rc = stage_in(reinterpret_cast<unsigned long long *>(rows), (size_t)n * (7 + H.W), false, S, &d_rows,
+                          hr)) return rc;
+    any_host = hr;
+    if (n > 0) {
+      k_hist_pack<<<(unsigned)std::min<int64_t>(256, (n + 255) / 256), 256, 0, st>>>(H, slots, n, d_rows);
+      CK(cudaGetLastError());
+      if (hr) CK(cudaMemcpyAsync(rows, d_rows, (size_t)n * (7 + H.W) * 8, cudaMemcpyDeviceToHost, st));
+    }
+    if (tallies) {
+      CK(cudaMemcpyAsync(tallies, H.tallies, (size_t)H.q * 5 * 8, cudaMemcpyDefault, st));
+      any_host = any_host || !is_device_ptr(tallies);
+    }
+  }
+  if (any_host) CK(cudaStreamSynchronize(st));
+  if (n_out) *n_out = n;
+  return 0;
+}
+
+int tv_hist_replace_rows(tv_hist *h, int64_t n, const uint64_t *rows, const int64_t *tallies, void *stream) {
+  if (!h) return fail(TV_ERR_ARG, "null histogram");
+  if (n < 0) return fail(TV_ERR_ARG, "negative n");
+  cudaStream_t st = (cudaStream_t)stream;
+  HistDev &H = h->H;
+  bool any_host = false;
+  {
+    Scratch S(st);
+    const bool keep = h->has_params;  // the enumeration parameters survive (payload fix-up at export)
+    if (int rc = tv_hist_clear(h, stream)) return rc;
+    h->has_params = keep;
+    if (tallies) {
+      long long *dt;
+      CK(S.get(&dt, (size_t)H.q * 5));
+      CK(cudaMemcpyAsync(dt, tallies, (size_t)H.q * 5 * 8, cudaMemcpyDefault, st));
+      k_hist_merge<<<1, 256, 0, st>>>(H, 0, HistRecords{}, dt);
+      CK(cudaGetLastError());
+      any_host = !is_device_ptr(tallies);
+    }
+    if (n > 0) {
+      unsigned long long *d_rows, *pmin;
+      int64_t *slot_of;
+      bool hr;
+      if (int rc = stage_in(reinterpret_cast<const unsigned long long *>(rows), (size_t)n * (7 + H.W), true, S,
+                            &d_rows, hr)) return rc;
+      any_host = any_host || hr;
+      CK(S.get(&pmin, (size_t)H.cap));
+      CK(S.get(&slot_of, (size_t)n));
+      CK(cudaMemsetAsync(pmin, 0xFF, (size_t)H.cap * 8, st));
+      const unsigned blocks = (unsigned)std::min<int64_t>(1024, (n + 255) / 256);
+      k_hist_merge_rows1<<<blocks, 256, 0, st>>>(H, n, d_rows, pmin, slot_of);
+      k_hist_merge_rows2<<<blocks, 256, 0, st>>>(H, n, d_rows, pmin, slot_of);
+      CK(cudaGetLastError());
+    }
+  }
+  if (any_host) CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
 int tv_hist_merge(tv_hist *h, int64_t n, const uint32_t *keys, const uint64_t *det, const uint64_t *steric,
                   const uint64_t *rep_det, const uint64_t *rep_any, const uint8_t *w, const uint8_t *hh,
                   const uint16_t *cells, const uint64_t *shape, const int64_t *tallies, void *stream) {

@@ -165,6 +165,54 @@ __global__ void k_hist_payload(HistDev H, const uint32_t *slots, const unsigned 
   }
 }
 
+// Packed raw records for the multi-GPU exchange: row = {key, det, steric, rep_det,
+// rep_any, pay_idx, whc, shape[W]} (7 + W u64), payload still the claimer's.
+__global__ void k_hist_pack(HistDev H, const uint32_t *slots, int64_t n, unsigned long long *rows) {
+  const int64_t R = 7 + H.W;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = slots[i];
+    unsigned long long *r = rows + i * R;
+    r[0] = H.keys[s]; r[1] = H.det[s]; r[2] = H.steric[s]; r[3] = H.rep_det[s]; r[4] = H.rep_any[s];
+    r[5] = H.pay_idx[s]; r[6] = H.whc[s];
+    for (int j = 0; j < H.W; j++) r[7 + j] = H.shape[s * H.W + j];
+  }
+}
+
+// Merge packed rows (several rows may share a key: one per rank).  Pass 1 adds the
+// counts, lowers the representatives and the per-slot minimum incoming payload owner
+// (pmin); pass 2 lets the row holding that owner write the payload if it beats the
+// slot's own.  Payload owners are genome indices, distinct across ranks.
+__global__ void k_hist_merge_rows1(HistDev H, int64_t n, const unsigned long long *rows, unsigned long long *pmin,
+                                   int64_t *slot_of) {
+  const int64_t R = 7 + H.W;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long *r = rows + i * R;
+    if (r[0] == 0ULL) { slot_of[i] = -1; continue; }  // padding row (keys carry a 1 << 32 tag)
+    bool gnew = false;
+    const int64_t g = hist_claim(H, (uint32_t)r[0], gnew);
+    slot_of[i] = g;
+    if (g < 0) continue;
+    if (r[1]) atomicAdd(&H.det[g], r[1]);
+    if (r[2]) atomicAdd(&H.steric[g], r[2]);
+    if (r[3] != ~0ULL) hist_min(&H.rep_det[g], r[3]);
+    if (r[4] != ~0ULL) hist_min(&H.rep_any[g], r[4]);
+    if (r[5] != ~0ULL) atomicMin(&pmin[g], r[5]);
+  }
+}
+__global__ void k_hist_merge_rows2(HistDev H, int64_t n, const unsigned long long *rows,
+                                   const unsigned long long *pmin, const int64_t *slot_of) {
+  const int64_t R = 7 + H.W;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = slot_of[i];
+    if (g < 0) continue;
+    const unsigned long long *r = rows + i * R;
+    if (r[5] == ~0ULL || r[5] != pmin[g] || r[5] >= H.pay_idx[g]) continue;
+    H.whc[g] = (uint32_t)r[6];
+    for (int j = 0; j < H.W; j++) H.shape[g * H.W + j] = r[7 + j];
+    H.pay_idx[g] = r[5];
+  }
+}
+
 struct HistRecords {  // SoA record arrays (device)
   uint32_t *keys;
   unsigned long long *det, *steric, *rep_det, *rep_any;

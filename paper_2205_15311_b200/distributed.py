@@ -18,7 +18,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .classify import DeviceHistogram, Histogram, _space_meta, chunk_plan, shape_words_for
+from .classify import DeviceHistogram, Histogram, _space_meta, chunk_plan, shape_words_for  # noqa: F401
 
 I64_MAX = np.iinfo(np.int64).max
 I64_MIN = np.iinfo(np.int64).min
@@ -96,6 +96,30 @@ def allreduce_histogram(h: Histogram, group=None) -> Histogram:
     return out
 
 
+def allreduce_device_histogram(dev: DeviceHistogram, group=None, meta: dict | None = None) -> Histogram:
+    """Device-resident exchange (NCCL): every rank packs its raw records on the GPU, one
+    all_gather moves them over NVLink, one all_reduce sums the tallies, and each rank
+    merges all rows into its own device histogram (tv_hist_replace_rows: counts added,
+    representatives lowered, payload = lowest owner) before the export re-derives the
+    payloads whose owner is not the representative.  Same result as allreduce_histogram."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    n_local, _ = dev.count()
+    dv = torch.device("cuda", torch.cuda.current_device())
+    nmax = torch.tensor([n_local], dtype=torch.int64, device=dv)
+    dist.all_reduce(nmax, op=dist.ReduceOp.MAX, group=group)
+    nmax = max(1, int(nmax.item()))
+    rows = torch.zeros((nmax, dev.row_width), dtype=torch.int64, device=dv)
+    tallies = torch.zeros((len(dev.ks), 5), dtype=torch.int64, device=dv)
+    dev.pack_into(rows, tallies)
+    allrows = torch.empty((world * nmax, dev.row_width), dtype=torch.int64, device=dv)
+    dist.all_gather_into_tensor(allrows, rows, group=group)
+    dist.all_reduce(tallies, op=dist.ReduceOp.SUM, group=group)
+    dev.replace_rows(allrows, tallies)
+    return dev.export(meta=meta)
+
+
 def rank_chunks(plan: list, rank: int, world: int) -> list:
     """Round-robin assignment of enumeration chunks to ranks."""
     return [c for i, c in enumerate(plan) if i % world == rank]
@@ -116,9 +140,11 @@ def enumerate_space_distributed(space, d: int = 19, k: int = 8, seed: int = 0, b
     try:
         for s, n in plan:
             dev.enumerate_range(space, s, n, d, seed, strict)
-        local = dev.export(meta=_space_meta(space, d, seed, strict))
+        if dist.get_backend(group) == "nccl":
+            out = allreduce_device_histogram(dev, group, meta=_space_meta(space, d, seed, strict))
+        else:
+            out = allreduce_histogram(dev.export(meta=_space_meta(space, d, seed, strict)), group)
     finally:
         dev.close()
-    out = allreduce_histogram(local, group)
     out.meta.update(start=int(start), count=int(count), world=world)
     return out

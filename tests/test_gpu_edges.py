@@ -158,3 +158,37 @@ def test_spec_acceptance_7_csv_byte_identical(M):
     plan = C.chunk_plan(0x300000, 1 << 19, 1 << 15)[::-1]  # reversed chunk order
     c = C.enumerate_space(sp, ks=(1, 2, 4, 8), start=0x300000, count=1 << 19, chunks=plan).to_csv()
     assert a.encode() == b.encode() == c.encode()
+
+
+@pytest.mark.parametrize("space,ks,chunk", [("s28", (1, 2, 4, 8), 1 << 18), ("s32", (7,), 1 << 20)])
+def test_device_exchange_rows_equal_single_histogram(M, space, ks, chunk):
+    """The multi-GPU exchange on one GPU: R 'ranks' enumerate round-robin chunks into their own
+    device histograms, pack raw rows (payload = claimer, no fix-up), and one histogram merges
+    all rows (tv_hist_replace_rows) -> its export equals the single-histogram enumeration,
+    payloads included (lowest owner wins, stale payloads re-derived at export)."""
+    import torch
+    K, L, C, Gm = M
+    sp = Gm.SearchSpace(2, 8) if space == "s28" else Gm.space_from_preset("s32_3_8")
+    start, count, R = (0, 1 << 22, 3) if space == "s28" else (0x9E370000, 1 << 22, 4)
+    plan = C.chunk_plan(start, count, chunk)
+    full = C.DeviceHistogram(ks, ks[-1], 5, 1 << 20)
+    for s, n in plan:
+        full.enumerate_range(sp, s, n, 19, 0, True)
+    exp = full.export()
+    parts = []
+    for r in range(R):
+        dh = C.DeviceHistogram(ks, ks[-1], 5, 1 << 20)
+        for s, n in plan[r::R]:
+            dh.enumerate_range(sp, s, n, 19, 0, True)
+        parts.append(dh)
+    rows, tal = [], torch.zeros((len(ks), 5), dtype=torch.int64, device="cuda")
+    for dh in parts:
+        n = dh.count()[0]
+        rr = torch.zeros((n + 7, dh.row_width), dtype=torch.int64, device="cuda")  # + padding rows
+        t = torch.zeros((len(ks), 5), dtype=torch.int64, device="cuda")
+        assert dh.pack_into(rr, t) == n
+        rows.append(rr)
+        tal += t
+    parts[1].replace_rows(torch.cat(rows), tal)
+    got = parts[1].export()
+    assert got == exp
