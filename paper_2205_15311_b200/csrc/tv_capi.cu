@@ -185,7 +185,8 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
     // per-CTA phenotype cache: 256 slots (with the behaviour-sorted order a CTA sees many
     // phenotypes of alike genomes: S28 32.3 -> 31.6 ms vs 128 slots; 512 halves occupancy)
     P.cta_slots = P.hist_mode ? (ec ? atoi(ec) : 256) : 0;
-    int threads = eth ? std::min(atoi(eth), TV_FAST_MAXT) & ~31 : TV_FAST_MAXT;
+    const int maxt = P.a == 3 ? fast_threads<3>() : fast_threads<2>();
+    int threads = eth ? std::min(atoi(eth), maxt) & ~31 : maxt;
     if (es) {
       P.S = std::max(4, atoi(es)) & ~1;
     } else {  // largest shared movelist part (<= 64 entries) that keeps two CTAs per SM

@@ -255,8 +255,13 @@ enum { ST_NEED = 0, ST_RUN = 1, ST_DONE = 2 };
 #ifndef TV_FAST_MAXT
 #define TV_FAST_MAXT 384  // 2 x 384 lanes per SM: 24 warps at <= 80 registers (measured +10% vs 2 x 256)
 #endif
+#ifndef TV_FAST_MAXT3
+#define TV_FAST_MAXT3 320  // a = 3: 64-bit candidate planes need 96 registers (S32 block 34.7 -> 33.7 ms)
+#endif
+template <int A> constexpr int fast_threads() { return A == 3 ? TV_FAST_MAXT3 : TV_FAST_MAXT; }
+
 template <int A, bool STRICT>
-__global__ void __launch_bounds__(TV_FAST_MAXT, TV_FAST_MINB) k_classify_fast(const __grid_constant__ ClassifyParams P) {
+__global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fast(const __grid_constant__ ClassifyParams P) {
   constexpr int NC = 4 * A;
   extern __shared__ uint32_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
