@@ -249,6 +249,9 @@ enum { ST_NEED = 0, ST_RUN = 1, ST_DONE = 2 };
 #endif
 #define TV_KEY_BITS (TV_KEY_TF ? 11 : 10)  // width of the k_prepass behaviour key
 
+#ifndef TV_PREPASS_MINB
+#define TV_PREPASS_MINB 3  // k_prepass at <= 80 registers (3 CTAs of 256 per SM)
+#endif
 #ifndef TV_FAST_MINB
 #define TV_FAST_MINB 2
 #endif
@@ -651,7 +654,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
 //    Results cannot depend on the order (per-genome substreams, commutative
 //    histogram updates).
 template <int A, bool STRICT>
-__global__ void __launch_bounds__(256) k_prepass(const __grid_constant__ ClassifyParams P, uint32_t *flags,
+__global__ void __launch_bounds__(256, TV_PREPASS_MINB) k_prepass(const __grid_constant__ ClassifyParams P, uint32_t *flags,
                                                  uint16_t *key_out, uint32_t *iota_out) {
   constexpr int NC = 4 * A;
   const int64_t nw = (P.n + 31) >> 5;
