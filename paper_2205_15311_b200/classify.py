@@ -445,6 +445,17 @@ class DeviceHistogram:
             int(start), int(count), a, bpl, _lib.ptr(mp), _lib.ptr(mv), mp.shape[0], _lib.ptr(fp), fp.shape[0],
             int(d), _lib.ptr(ks), ks.shape[0], self.hist_k, int(np.uint64(seed)), int(bool(strict)), self._h, stream))
 
+    def enumerate_chunks(self, space: SearchSpace, start: int, count: int, chunk: int, stride: int, d: int, seed: int,
+                         strict: bool, stream=None) -> None:
+        """``count`` items in chunks of ``chunk`` consecutive indices, chunk c starting at
+        start + c * stride: one launch for a rank's round-robin share (tv_enumerate_chunks)."""
+        a, bpl, mp, mv, fp = space.kernel_args()
+        ks = np.array(self.ks, np.int64)
+        _lib.check(_lib.lib().tv_enumerate_chunks(
+            int(start), int(count), int(chunk), int(stride), a, bpl, _lib.ptr(mp), _lib.ptr(mv), mp.shape[0],
+            _lib.ptr(fp), fp.shape[0], int(d), _lib.ptr(ks), ks.shape[0], self.hist_k, int(np.uint64(seed)),
+            int(bool(strict)), self._h, stream))
+
     def enumerate_indices(self, space: SearchSpace, indices, d: int, seed: int, strict: bool, stream=None) -> None:
         a, bpl, mp, mv, fp = space.kernel_args()
         ks = np.array(self.ks, np.int64)
@@ -541,7 +552,7 @@ def chunk_plan(start: int, count: int, batch_size: int) -> list[tuple[int, int]]
     return [(s, min(batch_size, start + count - s)) for s in range(start, start + count, batch_size)]
 
 
-def enumerate_space(space: SearchSpace, d: int = 19, k: int = 8, seed: int = 0, batch_size: int = 1 << 22,
+def enumerate_space(space: SearchSpace, d: int = 19, k: int = 8, seed: int = 0, batch_size: int = 1 << 26,
                     workers: int | None = None, *, ks=None, hist_k: int | None = None, strict: bool = True,
                     start: int = 0, count: int | None = None, capacity: int = 1 << 20,
                     checkpoint: str | None = None, checkpoint_every: int = 64, resume: str | None = None,

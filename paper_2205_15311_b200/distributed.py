@@ -125,7 +125,7 @@ def rank_chunks(plan: list, rank: int, world: int) -> list:
     return [c for i, c in enumerate(plan) if i % world == rank]
 
 
-def enumerate_space_distributed(space, d: int = 19, k: int = 8, seed: int = 0, batch_size: int = 1 << 22, *,
+def enumerate_space_distributed(space, d: int = 19, k: int = 8, seed: int = 0, batch_size: int = 1 << 20, *,
                                 ks=None, hist_k: int | None = None, strict: bool = True, start: int = 0,
                                 count: int | None = None, capacity: int = 1 << 20, group=None) -> Histogram:
     """enumerate_space over all ranks of ``group`` (one GPU per rank)."""
@@ -138,8 +138,14 @@ def enumerate_space_distributed(space, d: int = 19, k: int = 8, seed: int = 0, b
     plan = rank_chunks(chunk_plan(start, count, batch_size), rank, world)
     dev = DeviceHistogram(ks, hist_k, shape_words_for(d), capacity)
     try:
+        # the rank's full chunks in one strided launch (one kernel tail), a partial last chunk apart
+        full = [(s, n) for s, n in plan if n == batch_size]
+        if full:
+            dev.enumerate_chunks(space, full[0][0], len(full) * batch_size, batch_size, batch_size * world, d, seed,
+                                 strict)
         for s, n in plan:
-            dev.enumerate_range(space, s, n, d, seed, strict)
+            if n != batch_size:
+                dev.enumerate_range(space, s, n, d, seed, strict)
         if dist.get_backend(group) == "nccl":
             out = allreduce_device_histogram(dev, group, meta=_space_meta(space, d, seed, strict))
         else:
