@@ -29,10 +29,6 @@
 
 namespace tvb {
 
-#ifndef TV_WIDE_LABEL
-#define TV_WIDE_LABEL 1  // compare-free neighbour label reads (S28 -1.8 %)
-#endif
-
 template <typename M> __device__ __forceinline__ M rep_nib(uint32_t v) {
   return (M)v * (M)0x1111111111111111ULL;
 }
@@ -131,19 +127,12 @@ template <typename M, int NC, bool STRICT> struct CandSwar {
   // (>= NC: empty, shows no label); strict: a nonzero face against a nonzero
   // non-partner label excludes the candidate (_k:176-198)
   __device__ __forceinline__ M cand(uint32_t vN, uint32_t vE, uint32_t vS, uint32_t vW) const {
-#if TV_WIDE_LABEL
     // board values are < 16; nibbles >= NC of the zero-extended tables are 0, so an empty
     // neighbour (0xE / 0xF) reads label 0 without a compare
     const uint32_t pN = (uint32_t)(((uint64_t)E2 >> (4 * vN)) & 15u);
     const uint32_t pE = (uint32_t)(((uint64_t)E3 >> (4 * vE)) & 15u);
     const uint32_t pS = (uint32_t)(((uint64_t)E0 >> (4 * vS)) & 15u);
     const uint32_t pW = (uint32_t)(((uint64_t)E1 >> (4 * vW)) & 15u);
-#else
-    const uint32_t pN = vN < (uint32_t)NC ? get_nib<M>(E2, vN) : 0u;
-    const uint32_t pE = vE < (uint32_t)NC ? get_nib<M>(E3, vE) : 0u;
-    const uint32_t pS = vS < (uint32_t)NC ? get_nib<M>(E0, vS) : 0u;
-    const uint32_t pW = vW < (uint32_t)NC ? get_nib<M>(E1, vW) : 0u;
-#endif
     const M l7 = (M)0x7777777777777777ULL;
     M bond = 0, conf = 0;
 #define TV_DIR(Pd, Nd, p)                                                    \
@@ -241,13 +230,7 @@ template <bool S> struct Cand<1, S> : CandSwar<uint32_t, 8, S> {};
 
 enum { ST_NEED = 0, ST_RUN = 1, ST_DONE = 2 };
 
-#ifndef TV_MARK_ATOMIC
-#define TV_MARK_ATOMIC 1  // board updates of the pop loop as single shared atomics (S28 -1.8 %)
-#endif
-#ifndef TV_KEY_TF
-#define TV_KEY_TF 2  // trivial-freedom as the lowest key bit (S28 31.4 -> 31.0 ms; 1 = top bit, 0 = off)
-#endif
-#define TV_KEY_BITS (TV_KEY_TF ? 11 : 10)  // width of the k_prepass behaviour key
+#define TV_KEY_BITS 11  // width of the k_prepass behaviour key
 
 #ifndef TV_PREPASS_MINB
 #define TV_PREPASS_MINB 3  // k_prepass at <= 80 registers (3 CTAs of 256 per SM)
@@ -577,13 +560,9 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
       else if (r == 1 || c == 1 || r == d || c == d) pend = RUN_UNBOUND;     // _k:212-213
       else place = true;
     }
-#if TV_MARK_ATOMIC
     // a popped cell always holds 0xE (on the movelist), so one XOR writes the placed
     // candidate or 0xF (drop, re-pushable, _k:210-211); the word is lane-private
     atomicXor(&Ln.gw[(lin >> 3) * 32], (0xEu ^ (place ? cf : 0xFu)) << ((lin & 7) * 4));
-#else
-    Ln.set_nib(lin, place ? cf : 0xFu);  // place, or drop (re-pushable, _k:210-211)
-#endif
     if (!place) continue;
     minr = min(minr, r); maxr = max(maxr, r);                                 // _k:217-224
     minc = min(minc, c); maxc = max(maxc, c);
@@ -612,11 +591,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
         const int dl = (dir & 1u) ? 1 : PD;
         const int nl = ((dir + 1u) & 2u) ? lin + dl : lin - dl;
         Ln.st_write(sp + j, (uint32_t)nl);
-#if TV_MARK_ATOMIC
         atomicAnd(&Ln.gw[(nl >> 3) * 32], ~(1u << ((nl & 7) * 4)));  // F -> E (one ATOMS, lane-private word)
-#else
-        Ln.gw[(nl >> 3) * 32] &= ~(1u << ((nl & 7) * 4));  // F -> E: on the movelist
-#endif
       }
     }
     sp += mm;
@@ -703,8 +678,7 @@ __global__ void __launch_bounds__(256, TV_PREPASS_MINB) k_prepass(const __grid_c
         }
         uint32_t kk = ((line ? 0u : 1u) << 9) | ((self0 ? 0u : 1u) << 8) | ((uint32_t)(4 - nb0) << 5) |
                       ((selfr ? 0u : 1u) << 4) | (uint32_t)(8 - nbr);
-        if (TV_KEY_TF == 1) kk |= (f ? 0u : 1u) << 10;
-        if (TV_KEY_TF == 2) kk = (kk << 1) | (f ? 0u : 1u);
+        kk = (kk << 1) | (f ? 0u : 1u);  // trivial-freedom (a <= 2) as the lowest key bit
         key_out[item] = (uint16_t)kk;
         iota_out[item] = (uint32_t)item;
       }
