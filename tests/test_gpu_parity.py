@@ -222,3 +222,26 @@ def test_enumerate_full_s32_histogram(K):
     for k, v in cols.items():
         assert np.array_equal(v[sel], smp[k]), k
         assert hashlib.sha256(np.ascontiguousarray(v).tobytes()).hexdigest() == meta["sha256"][k], k
+
+
+@pytest.mark.parametrize("seed,strict", [(2205, True), (7, False)])
+def test_enumerate_full_s28_other_seeds_vs_oracle(K, seed, strict):
+    """Full S_{2,8} at a seed and contact rule the reference goldens do not cover: device histogram
+    (behaviour-sorted order, early cut-off, payload fix-up) == the oracle's per-genome rows
+    aggregated on the host, every record column."""
+    from oracle import oracle as O
+    from paper_2205_15311_b200.classify import Histogram, enumerate_space
+    from paper_2205_15311_b200.genome import SearchSpace
+    ks = (1, 2, 4, 8)
+    h = enumerate_space(SearchSpace(2, 8), d=19, ks=ks, seed=seed, strict=strict, batch_size=1 << 24)
+    acc = None
+    blk = 1 << 22
+    for s in range(0, 1 << 24, blk):
+        idx = np.arange(s, s + blk, dtype=np.uint64)
+        o = G.fresh_outputs(blk, 4)
+        O.classify_batch(idx, *S28_ARGS, 19, np.array(ks), 8, seed, strict, *[o[k] for k in G.OUT_KEYS])
+        part = Histogram.from_rows(idx, *[o[k] for k in G.OUT_KEYS], ks=ks, hist_k=8, W=5)
+        acc = part if acc is None else acc.merge(part)
+    for k in ("keys", "det", "steric", "rep_det", "rep_any", "w", "h", "cells", "tallies"):
+        assert np.array_equal(getattr(h, k).astype(np.int64), getattr(acc, k).astype(np.int64)), k
+    assert np.array_equal(h.shape, acc.shape)
