@@ -31,13 +31,14 @@ __host__ __device__ __forceinline__ uint64_t stream_state(uint64_t seed, uint64_
 // counter-based draw: advance then mix; bounded draw uses the high word (_k:51-60).
 // Only the high 32 bits of the mixed value are consumed, so the last xor-shift
 // is evaluated on the high word alone.
-__device__ __forceinline__ uint32_t rng_below(uint64_t &s, uint32_t n) {
-  s += kGold;
-  uint64_t z = s;
+__device__ __forceinline__ uint32_t rng_hi(uint64_t z) {  // high word of mix64(z)
   z = (z ^ (z >> 30)) * kMixA;
   z = (z ^ (z >> 27)) * kMixB;
-  const uint32_t hi = (uint32_t)(z >> 32) ^ (uint32_t)(z >> 63);
-  return __umulhi(hi, n);
+  return (uint32_t)(z >> 32) ^ (uint32_t)(z >> 63);
+}
+__device__ __forceinline__ uint32_t rng_below(uint64_t &s, uint32_t n) {
+  s += kGold;
+  return __umulhi(rng_hi(s), n);
 }
 
 // one-at-a-time hash steps (_k:65-76)

@@ -573,15 +573,16 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
     if (vE == 0xFu) { nbp |= 1u << (8 * m); m++; }
     if (vS == 0xFu) { nbp |= 2u << (8 * m); m++; }
     if (vW == 0xFu) { nbp |= 3u << (8 * m); m++; }
-    if (m == 3) {                                                              // Fisher-Yates (_k:238-242)
-      const uint32_t q = rng_below(rs, 3u);
-      const uint32_t x = ((nbp >> 16) ^ (nbp >> (8 * q))) & 0xFFu;
-      nbp ^= (x << 16) | (x << (8 * q));
-    }
-    if (m >= 2) {
-      const uint32_t q = rng_below(rs, 2u);
-      const uint32_t x = ((nbp >> 8) ^ (nbp >> (8 * q))) & 0xFFu;
-      nbp ^= (x << 8) | (x << (8 * q));
+    if (m >= 2) {  // Fisher-Yates (_k:238-242): both draws of m == 3 mixed side by side
+      const bool three = m == 3;
+      const uint32_t h1 = rng_hi(rs + kGold), h2 = rng_hi(rs + 2 * kGold);
+      rs += three ? 2 * kGold : kGold;
+      const uint32_t q3 = three ? __umulhi(h1, 3u) : 2u;  // m == 2: swap 2 with itself
+      uint32_t x = ((nbp >> 16) ^ (nbp >> (8 * q3))) & 0xFFu;
+      nbp ^= (x << 16) | (x << (8 * q3));
+      const uint32_t q2 = (three ? h2 : h1) >> 31;  // below(2) = high bit
+      x = ((nbp >> 8) ^ (nbp >> (8 * q2))) & 0xFFu;
+      nbp ^= (x << 8) | (x << (8 * q2));
     }
     const int mm = min(m, dd - sp);  // capacity check before each push (_k:243-245)
 #pragma unroll
