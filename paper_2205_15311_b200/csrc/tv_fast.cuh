@@ -296,11 +296,10 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
   bool tfree = false;  // no run of this genome can go TRIVIAL (k_prepass)
   Cand<A, STRICT> K;
 
+  int nlive = 32;  // lanes not DONE (warp-uniform; lanes only finish in the refill below)
   for (;;) {
-    const unsigned live = __ballot_sync(0xFFFFFFFFu, st != ST_DONE);
-    if (live == 0) break;
     const unsigned parked = __ballot_sync(0xFFFFFFFFu, st == ST_NEED || pend >= 0);
-    const int nlive = __popc(live), npark = __popc(parked);
+    const int npark = __popc(parked);
     if (npark > 0 && (npark >= min(thresh, (nlive + 1) >> 1) || npark == nlive)) {
       // =================== service pass over parked lanes ===================
       bool start = false;
@@ -540,6 +539,8 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
         }
         sp = 4;
       }
+      nlive = __popc(__ballot_sync(0xFFFFFFFFu, st != ST_DONE));
+      if (nlive == 0) break;
     }
     if (st != ST_RUN || pend >= 0) continue;
 
