@@ -296,11 +296,12 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
   bool tfree = false;  // no run of this genome can go TRIVIAL (k_prepass)
   Cand<A, STRICT> K;
 
-  int nlive = 32;  // lanes not DONE (warp-uniform; lanes only finish in the refill below)
+  // lanes not DONE (warp-uniform; lanes only finish in the refill below) and the parked-lane
+  // count that triggers a service pass: min(thresh, half the live lanes), so never above nlive
+  int nlive = 32, trig = min(thresh, 16);
   for (;;) {
     const unsigned parked = __ballot_sync(0xFFFFFFFFu, st == ST_NEED || pend >= 0);
-    const int npark = __popc(parked);
-    if (npark > 0 && (npark >= min(thresh, (nlive + 1) >> 1) || npark == nlive)) {
+    if (__popc(parked) >= trig) {
       // =================== service pass over parked lanes ===================
       bool start = false;
       if (pend >= 0) {
@@ -541,14 +542,11 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
       }
       nlive = __popc(__ballot_sync(0xFFFFFFFFu, st != ST_DONE));
       if (nlive == 0) break;
+      trig = min(thresh, (nlive + 1) >> 1);
     }
     if (st != ST_RUN || pend >= 0) continue;
 
     // =================== one movelist pop (_k:138-248) ===================
-    if (sp == 0) {
-      pend = RUN_BOUNDED;
-      continue;
-    }
     const int lin = (int)Ln.st_read(--sp);
     const uint32_t vN = Ln.nib(lin - PD), vE = Ln.nib(lin + 1);
     const uint32_t vS = Ln.nib(lin + PD), vW = Ln.nib(lin - 1);
@@ -564,7 +562,10 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
     // a popped cell always holds 0xE (on the movelist), so one XOR writes the placed
     // candidate or 0xF (drop, re-pushable, _k:210-211); the word is lane-private
     atomicXor(&Ln.gw[(lin >> 3) * 32], (0xEu ^ (place ? cf : 0xFu)) << ((lin & 7) * 4));
-    if (!place) continue;
+    if (!place) {
+      if (pend < 0 && sp == 0) pend = RUN_BOUNDED;  // movelist exhausted (_k:138, 249)
+      continue;
+    }
     minr = min(minr, r); maxr = max(maxr, r);                                 // _k:217-224
     minc = min(minc, c); maxc = max(maxc, c);
     // new frontier N,E,S,W (_k:225-237) as 2-bit direction codes, one per byte
@@ -598,6 +599,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
     }
     sp += mm;
     if (mm < m) pend = RUN_OVERFLOW;
+    else if (sp == 0) pend = RUN_BOUNDED;
   }
 
   if (P.hist_mode) {
