@@ -157,7 +157,7 @@ int fill_common(int32_t a, int32_t bpl, const int64_t *mask_pos, const uint8_t *
   C.P.a = a; C.P.d = d; C.P.strict = strict ? 1 : 0; C.P.q = (int32_t)q; C.P.kmax = kmax; C.P.hist_k = hist_k;
   C.P.seed = seed;
   const int PD = d + 2;
-  C.fast = a <= 3 && bpl <= 3 && PD * PD < 65536 && PD < 256;
+  C.fast = a <= 3 && bpl <= 3 && PD * ((PD + 7) / 8) * 8 < 65536 && PD < 256;  // cell ids fit u16
   return 0;
 }
 
@@ -176,12 +176,12 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
   P.work = work;
   const int d = P.d, dd = d * d;
   if (C.fast) {
-    const int PD = d + 2;
-    P.GW = (PD * PD + 7) / 8;
+    P.GW = fast_board_words(P.a, d);
     // tunables (env overrides exist for A/B measurements only)
     const char *es = getenv("TV_STACK_S"), *ec = getenv("TV_CTA_SLOTS"), *et = getenv("TV_SERVICE_THRESH");
     const char *eth = getenv("TV_FAST_THREADS");
-    P.service_thresh = et ? atoi(et) : 0;
+    // parked lanes that trigger a service pass (measured: a = 2 best at 12, a = 3 at 20)
+    P.service_thresh = et ? atoi(et) : (P.a == 3 ? 20 : 12);
     // per-CTA phenotype cache: 256 slots (with the behaviour-sorted order a CTA sees many
     // phenotypes of alike genomes: S28 32.3 -> 31.6 ms vs 128 slots; 512 halves occupancy)
     P.cta_slots = P.hist_mode ? (ec ? atoi(ec) : 256) : 0;
@@ -191,7 +191,7 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
       P.S = std::max(4, atoi(es)) & ~1;
     } else {  // largest shared movelist part (<= 64 entries) that keeps two CTAs per SM
       P.S = 64;
-      while (P.S > 16 && 2 * (fast_smem_bytes(threads, P.GW, P.S, P.cta_slots, P.q) + 1024) > 228 * 1024) P.S -= 2;
+      while (P.S > 8 && 2 * (fast_smem_bytes(threads, P.GW, P.S, P.cta_slots, P.q) + 1024) > 228 * 1024) P.S -= 2;
     }
     P.S = std::max(4, std::min(P.S, (dd + 1) & ~1));
     P.spill_cap = std::max(0, dd - P.S);

@@ -230,6 +230,13 @@ template <bool S> struct Cand<1, S> : CandSwar<uint32_t, 8, S> {};
 
 enum { ST_NEED = 0, ST_RUN = 1, ST_DONE = 2 };
 
+// board layout of the fast kernel: row-aligned (a <= 2) or dense (a = 3), see k_classify_fast
+template <int A> __host__ __device__ constexpr bool fast_rows() { return A <= 2; }
+__host__ __device__ inline int fast_board_words(int a, int d) {
+  const int PD = d + 2;
+  return a <= 2 ? PD * ((PD + 7) / 8) : (PD * PD + 7) / 8;
+}
+
 #define TV_KEY_BITS 11  // width of the k_prepass behaviour key
 
 #ifndef TV_PREPASS_MINB
@@ -280,9 +287,13 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
   for (int w = 0; w < P.GW; w++) Ln.gw[w * 32] = 0xFFFFFFFFu;
   __syncthreads();
 
-  const int d = P.d, PD = d + 2, dd = d * d;
-  const uint32_t magic = (uint32_t)(0x100000000ULL / (uint64_t)PD) + 1u;
-  const int cr = (d >> 1) + 1, centre = cr * PD + cr;
+  // board row stride RS nibbles, cell (r, c) = nibble lin = r RS + c.  a <= 2: rows of RW whole
+  // words (RS = 8 RW >= d + 2), so the N and S neighbours sit RW words above / below in the same
+  // nibble position; a = 3: RS = d + 2 (dense; its service passes scan and clear fewer words)
+  constexpr bool ROWS = fast_rows<A>();
+  const int d = P.d, dd = d * d, RW = (d + 2 + 7) >> 3, RS = ROWS ? 8 * RW : d + 2;
+  const uint32_t magic = (uint32_t)(0x100000000ULL / (uint64_t)RS) + 1u;
+  const int cr = (d >> 1) + 1, centre = cr * RS + cr;
   const int thresh = P.service_thresh > 0 ? P.service_thresh : 16;
 
   int st = ST_NEED, pend = -1;
@@ -321,7 +332,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
           w = maxc - minc + 1;
           h = maxr - minr + 1;
           hs = oat_step(oat_step(0u, (uint32_t)w), (uint32_t)h);
-          const int lo = (minr * PD + minc) >> 3, hi = (maxr * PD + maxc) >> 3;
+          const int lo = (minr * RS + minc) >> 3, hi = (maxr * RS + maxc) >> 3;
           int64_t cw = 0;
           unsigned long long acc = 0;
           for (int wi = lo; wi <= hi; wi++) {
@@ -331,7 +342,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
               occ &= occ - 1;
               const uint32_t L = (uint32_t)(wi * 8 + (b >> 2));
               const uint32_t R = __umulhi(L, magic);
-              const int col = (int)(L - R * PD);
+              const int col = (int)(L - R * RS);
               const int y = (int)R - minr, x = col - minc;
               hs = oat_step(oat_step(hs, (uint32_t)x), (uint32_t)y);
               n++;
@@ -350,8 +361,8 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
           hs = oat_final(hs);
         }
         {  // clear: every tile and movelist mark lies inside bbox +- 1
-          const int lo = ((minr - 1) * PD + (minc - 1)) >> 3;
-          const int hi = ((maxr + 1) * PD + (maxc + 1)) >> 3;
+          const int lo = ((minr - 1) * RS + (minc - 1)) >> 3;
+          const int hi = ((maxr + 1) * RS + (maxc + 1)) >> 3;
           for (int wi = lo; wi <= hi; wi++) Ln.gw[wi * 32] = 0xFFFFFFFFu;
         }
         if (replay) {
@@ -533,7 +544,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
 #pragma unroll
         for (int j = 0; j < 4; j++) {
           const uint32_t dir = (nbp >> (8 * j)) & 3u;
-          const int dl = (dir & 1u) ? 1 : PD;
+          const int dl = (dir & 1u) ? 1 : RS;
           const int nl = ((dir + 1u) & 2u) ? centre + dl : centre - dl;
           Ln.st_write(j, (uint32_t)nl);
           Ln.set_nib(nl, 0xEu);
@@ -548,11 +559,14 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
 
     // =================== one movelist pop (_k:138-248) ===================
     const int lin = (int)Ln.st_read(--sp);
-    const uint32_t vN = Ln.nib(lin - PD), vE = Ln.nib(lin + 1);
-    const uint32_t vS = Ln.nib(lin + PD), vW = Ln.nib(lin - 1);
+    uint32_t *const pw = Ln.gw + (lin >> 3) * 32;  // the popped cell's word
+    const int sh = (lin & 7) * 4;
+    const uint32_t vN = ROWS ? (pw[-RW * 32] >> sh) & 15u : Ln.nib(lin - RS);
+    const uint32_t vS = ROWS ? (pw[RW * 32] >> sh) & 15u : Ln.nib(lin + RS);
+    const uint32_t vE = Ln.nib(lin + 1), vW = Ln.nib(lin - 1);
     const auto cand = K.cand(vN, vE, vS, vW);
     const uint32_t cf = K.first(cand);
-    const int r = (int)__umulhi((uint32_t)lin, magic), c = lin - r * PD;
+    const int r = (int)__umulhi((uint32_t)lin, magic), c = lin - r * RS;
     bool place = false;
     if (cand != 0) {
       if (K.ambiguous(cand, cf)) pend = RUN_TRIVIAL;                           // _k:208-209
@@ -561,7 +575,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
     }
     // a popped cell always holds 0xE (on the movelist), so one XOR writes the placed
     // candidate or 0xF (drop, re-pushable, _k:210-211); the word is lane-private
-    atomicXor(&Ln.gw[(lin >> 3) * 32], (0xEu ^ (place ? cf : 0xFu)) << ((lin & 7) * 4));
+    atomicXor(pw, (0xEu ^ (place ? cf : 0xFu)) << sh);
     if (!place) {
       if (pend < 0 && sp == 0) pend = RUN_BOUNDED;  // movelist exhausted (_k:138, 249)
       continue;
@@ -591,7 +605,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
     for (int j = 0; j < 3; j++) {
       if (j < mm) {
         const uint32_t dir = (nbp >> (8 * j)) & 3u;
-        const int dl = (dir & 1u) ? 1 : PD;
+        const int dl = (dir & 1u) ? 1 : RS;
         const int nl = ((dir + 1u) & 2u) ? lin + dl : lin - dl;
         Ln.st_write(sp + j, (uint32_t)nl);
         atomicAnd(&Ln.gw[(nl >> 3) * 32], ~(1u << ((nl & 7) * 4)));  // F -> E (one ATOMS, lane-private word)
