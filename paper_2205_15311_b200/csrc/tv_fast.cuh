@@ -561,9 +561,17 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
     const int lin = (int)Ln.st_read(--sp);
     uint32_t *const pw = Ln.gw + (lin >> 3) * 32;  // the popped cell's word
     const int sh = (lin & 7) * 4;
-    const uint32_t vN = ROWS ? (pw[-RW * 32] >> sh) & 15u : Ln.nib(lin - RS);
-    const uint32_t vS = ROWS ? (pw[RW * 32] >> sh) & 15u : Ln.nib(lin + RS);
-    const uint32_t vE = Ln.nib(lin + 1), vW = Ln.nib(lin - 1);
+    uint32_t vN, vS, vE, vW;
+    if (ROWS) {  // W / E from the own word or its neighbour word (a row never ends mid-word)
+      const uint32_t wm = pw[-32], w0 = pw[0], wp = pw[32];
+      vN = (pw[-RW * 32] >> sh) & 15u;
+      vS = (pw[RW * 32] >> sh) & 15u;
+      vW = ((sh ? w0 : wm) >> ((sh - 4) & 31)) & 15u;
+      vE = ((sh == 28 ? wp : w0) >> ((sh + 4) & 31)) & 15u;
+    } else {
+      vN = Ln.nib(lin - RS); vS = Ln.nib(lin + RS);
+      vE = Ln.nib(lin + 1); vW = Ln.nib(lin - 1);
+    }
     const auto cand = K.cand(vN, vE, vS, vW);
     const uint32_t cf = K.first(cand);
     const int r = (int)__umulhi((uint32_t)lin, magic), c = lin - r * RS;
