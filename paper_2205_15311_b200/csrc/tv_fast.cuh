@@ -123,16 +123,16 @@ template <typename M, int NC, bool STRICT> struct CandSwar {
     N2 = nz_nib<M>(E2) & VALID; N3 = nz_nib<M>(E3) & VALID;
   }
 
-  // candidates at a cell whose N,E,S,W neighbours hold board values vN..vW
+  // candidates at a cell whose N,E,S,W neighbours hold board values vN..vW, passed as 4 v
   // (>= NC: empty, shows no label); strict: a nonzero face against a nonzero
   // non-partner label excludes the candidate (_k:176-198)
-  __device__ __forceinline__ M cand(uint32_t vN, uint32_t vE, uint32_t vS, uint32_t vW) const {
+  __device__ __forceinline__ M cand(uint32_t sN, uint32_t sE, uint32_t sS, uint32_t sW) const {
     // board values are < 16; nibbles >= NC of the zero-extended tables are 0, so an empty
     // neighbour (0xE / 0xF) reads label 0 without a compare
-    const uint32_t pN = (uint32_t)(((uint64_t)E2 >> (4 * vN)) & 15u);
-    const uint32_t pE = (uint32_t)(((uint64_t)E3 >> (4 * vE)) & 15u);
-    const uint32_t pS = (uint32_t)(((uint64_t)E0 >> (4 * vS)) & 15u);
-    const uint32_t pW = (uint32_t)(((uint64_t)E1 >> (4 * vW)) & 15u);
+    const uint32_t pN = (uint32_t)(((uint64_t)E2 >> sN) & 15u);
+    const uint32_t pE = (uint32_t)(((uint64_t)E3 >> sE) & 15u);
+    const uint32_t pS = (uint32_t)(((uint64_t)E0 >> sS) & 15u);
+    const uint32_t pW = (uint32_t)(((uint64_t)E1 >> sW) & 15u);
     const M l7 = (M)0x7777777777777777ULL;
     M bond = 0, conf = 0;
 #define TV_DIR(Pd, Nd, p)                                                    \
@@ -561,16 +561,19 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
     const int lin = (int)Ln.st_read(--sp);
     uint32_t *const pw = Ln.gw + (lin >> 3) * 32;  // the popped cell's word
     const int sh = (lin & 7) * 4;
+    // neighbour values times 4 (0x3C = empty), each one rotate of its word: nibble at bit p
+    // lands at bits 2..5 after a right rotate by p - 2
     uint32_t vN, vS, vE, vW;
     if (ROWS) {  // W / E from the own word or its neighbour word (a row never ends mid-word)
       const uint32_t wm = pw[-32], w0 = pw[0], wp = pw[32];
-      vN = (pw[-RW * 32] >> sh) & 15u;
-      vS = (pw[RW * 32] >> sh) & 15u;
-      vW = ((sh ? w0 : wm) >> ((sh - 4) & 31)) & 15u;
-      vE = ((sh == 28 ? wp : w0) >> ((sh + 4) & 31)) & 15u;
+      vN = __funnelshift_r(pw[-RW * 32], pw[-RW * 32], (sh - 2) & 31) & 0x3Cu;
+      vS = __funnelshift_r(pw[RW * 32], pw[RW * 32], (sh - 2) & 31) & 0x3Cu;
+      const uint32_t ww = sh ? w0 : wm, we = sh == 28 ? wp : w0;
+      vW = __funnelshift_r(ww, ww, (sh - 6) & 31) & 0x3Cu;
+      vE = __funnelshift_r(we, we, (sh + 2) & 31) & 0x3Cu;
     } else {
-      vN = Ln.nib(lin - RS); vS = Ln.nib(lin + RS);
-      vE = Ln.nib(lin + 1); vW = Ln.nib(lin - 1);
+      vN = 4 * Ln.nib(lin - RS); vS = 4 * Ln.nib(lin + RS);
+      vE = 4 * Ln.nib(lin + 1); vW = 4 * Ln.nib(lin - 1);
     }
     const auto cand = K.cand(vN, vE, vS, vW);
     const uint32_t cf = K.first(cand);
@@ -593,10 +596,10 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
     // new frontier N,E,S,W (_k:225-237) as 2-bit direction codes, one per byte
     uint32_t nbp = 0;
     int m = 0;
-    if (vN == 0xFu) { nbp |= 0u << (8 * m); m++; }
-    if (vE == 0xFu) { nbp |= 1u << (8 * m); m++; }
-    if (vS == 0xFu) { nbp |= 2u << (8 * m); m++; }
-    if (vW == 0xFu) { nbp |= 3u << (8 * m); m++; }
+    if (vN == 0x3Cu) { nbp |= 0u << (8 * m); m++; }
+    if (vE == 0x3Cu) { nbp |= 1u << (8 * m); m++; }
+    if (vS == 0x3Cu) { nbp |= 2u << (8 * m); m++; }
+    if (vW == 0x3Cu) { nbp |= 3u << (8 * m); m++; }
     if (m >= 2) {  // Fisher-Yates (_k:238-242): both draws of m == 3 mixed side by side
       const bool three = m == 3;
       const uint32_t h1 = rng_hi(rs + kGold), h2 = rng_hi(rs + 2 * kGold);
