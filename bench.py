@@ -341,7 +341,7 @@ def ga_jatam_bench(n: int = 1 << 20, gens: int = 20) -> dict:
             "config": {"workload": "GA toward a 12-cell S_(2,8) target shape, population 2^20, L=24, k=8, d=19, "
                                    "muL=0.3, asexual, random initial population", "generations_timed": gens},
             "best_fitness_seen": best,
-            "note": "each generation = k_trivial_flags + k_classify_fast (fit mode) over 2^20 genomes + one "
+            "note": "each generation = k_prepass + key sort + k_classify_fast (fit mode) over 2^20 genomes + one "
                     "k_ga_run generation; timed with CUDA events on the launch stream"}
 
 
@@ -506,8 +506,9 @@ def main():
         roof = {"bound": "int32_alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tops/s",
                 "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read+write)",
                 "kernel": "k_classify_fast<2>", "kernel_ms": kms,
-                "kernel_ms_covers": "one tv_enumerate_chunks call: k_trivial_flags<2> pre-pass (~1 ms) + "
-                                    "k_classify_fast<2> (conservative: both kernels' time)",
+                "kernel_ms_covers": "one tv_enumerate_chunks call: k_prepass<2> (trivial-freedom bits + behaviour "
+                                    "key, ~1.3 ms) + CUB radix sort of the keys (~0.2 ms) + k_classify_fast<2> "
+                                    "(conservative: all three kernels' time)",
                 "ops_per_genome": ops_per_genome,
                 "peak_source": "measured on this GPU: tv_int_peak_launch (8 independent IADD3/LOP3 chains/thread)",
                 "ops_source": "event-weighted algorithmic int32 ops (SURVEY.md 8d weights) x oracle event counts, "

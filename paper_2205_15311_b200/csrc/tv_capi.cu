@@ -229,8 +229,8 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
       // behaviour-sorted processing order for every mode (outputs stay addressed by item):
       // see k_prepass.  Classify-type calls above 2^30 items keep item order (sort scratch).
       // TV_ORDER=0 disables it.
-      const bool want_order = (P.hist_mode || P.n <= ((int64_t)1 << 30)) && P.n >= 4096 &&
-                              (eo ? atoi(eo) != 0 : true);
+      const bool want_order = (P.hist_mode || P.n <= ((int64_t)1 << 30)) && P.n >= 4096 && !P.pay_mode &&
+                              (eo ? atoi(eo) != 0 : true);  // (payload-mode items are (record, run) pairs)
       // histogram mode runs in slices of <= 2^26 items (sort and flag scratch stay bounded;
       // the histogram accumulates across slices)
       const int64_t n_all = P.n, slice = P.hist_mode ? ((int64_t)1 << 26) : n_all;
@@ -379,23 +379,29 @@ int fix_payloads(tv_hist *h, cudaStream_t st) {
   if (!h->has_params)
     return fail(TV_ERR_ARG, "%u histogram records lack their representative's payload and no enumeration "
                             "parameters are known (merge complete records or enumerate into this histogram)", ns);
-  // Fast spaces: payload mode (replay the representative's runs until one reproduces
-  // the key, usually run 0).  Others: full classification of the representative,
-  // whose attributed row is the payload.
+  // Fast spaces: payload mode, every run < hist_k of every representative replayed in its own
+  // lane (the attributed run of a DET / STERIC genome lies below hist_k, _k:357-381) and the
+  // first run reproducing the key taken -- the latency of one run instead of a chain of runs.
+  // Others: full classification of the representative, whose attributed row is the payload.
   Common C = h->params;
   ClassifyParams &P = C.P;
-  P.hist_mode = 0; P.fit_mode = 0; P.indices = reinterpret_cast<const uint64_t *>(idx); P.n = ns;
+  int shift = 0;
+  while (C.fast && (1 << shift) < P.hist_k) shift++;
+  const int R = 1 << shift;  // runs >= hist_k only ever follow a matching run
+  const int64_t rows = (int64_t)ns * R;
+  P.hist_mode = 0; P.fit_mode = 0; P.indices = reinterpret_cast<const uint64_t *>(idx); P.n = rows;
   P.start = 0; P.chunk = 0; P.stride = 0;
   P.pay_mode = C.fast ? 1 : 0;
+  P.pay_shift = shift;
   P.pay_key = keys;
   uint8_t *cls, *w, *hh; uint32_t *hash; uint16_t *cells; unsigned long long *shape;
-  CK(S.get(&cls, (size_t)ns * P.q)); CK(S.get(&hash, ns)); CK(S.get(&w, ns)); CK(S.get(&hh, ns));
-  CK(S.get(&cells, ns)); CK(S.get(&shape, (size_t)ns * H.W));
+  CK(S.get(&cls, (size_t)rows * P.q)); CK(S.get(&hash, rows)); CK(S.get(&w, rows)); CK(S.get(&hh, rows));
+  CK(S.get(&cells, rows)); CK(S.get(&shape, (size_t)rows * H.W));
   P.out_class = cls; P.out_hash = hash; P.out_w = w; P.out_h = hh; P.out_cells = cells; P.out_shape = shape;
   P.W = H.W;
   if (int rc = launch_classify(C, S, st)) return rc;
   const int blocks = (int)std::min<int64_t>(256, ((int64_t)ns + 255) / 256);
-  k_hist_payload<<<blocks, 256, 0, st>>>(H, slots, idx, ns, hash, w, hh, cells, shape, cnt + 1);
+  k_hist_payload<<<blocks, 256, 0, st>>>(H, slots, idx, ns, R, hash, w, hh, cells, shape, cnt + 1);
   CK(cudaGetLastError());
   unsigned int err = 0;
   CK(cudaMemcpyAsync(&err, cnt + 1, 4, cudaMemcpyDeviceToHost, st));

@@ -375,18 +375,15 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
             P.hist.pay_idx[pslot] = idx;
           }
           st = ST_NEED;
-        } else if (P.pay_mode) {  // representative payload: first run reproducing the key
-          const uint32_t key = P.pay_key[item];
+        } else if (P.pay_mode) {  // representative payload: does this run reproduce the key?
+          const uint32_t key = P.pay_key[item >> P.pay_shift];
           if (ended == RUN_BOUNDED && hs == key) {
             P.out_hash[item] = hs;
             P.out_w[item] = (uint8_t)w; P.out_h[item] = (uint8_t)h; P.out_cells[item] = (uint16_t)n;
-            st = ST_NEED;
-          } else if (ended != RUN_TRIVIAL && ended != RUN_OVERFLOW && ++run < P.kmax) {
-            start = true;
           } else {
             P.out_hash[item] = ~key;
-            st = ST_NEED;
           }
+          st = ST_NEED;
         } else {
           // ---- fold one run (_k:323-349)
           bool done = false;
@@ -516,14 +513,15 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
             // behaviour-sorted processing order (k_prepass); every per-item output and flag below
             // is addressed by the item's own number, so the order is invisible to the caller
             if (P.order) item = (int64_t)P.order[item];
-            idx = item_index(P.indices, P.start, P.chunk, P.stride, P.item0 + item);
+            const int64_t rec = item >> P.pay_shift;  // payload mode: item = (record, run)
+            idx = item_index(P.indices, P.start, P.chunk, P.stride, P.item0 + rec);
             uint32_t lab[12];  // decode labels (_k:384-401)
 #pragma unroll
             for (int te = 0; te < 12; te++) lab[te] = te < NC ? decode_label(P.dec, te, idx) : 0u;
             K.build(lab, A);
             tfree = P.tf_flags ? ((P.tf_flags[item >> 5] >> (item & 31)) & 1u) != 0u : false;
             trivial_at = first_unbound = first_mismatch = -1;
-            run = 0;
+            run = (int)item & ((1 << P.pay_shift) - 1);
             replay = 0;
             start = true;
             st = ST_RUN;

@@ -153,14 +153,20 @@ __global__ void k_hist_stale(HistDev H, uint32_t *slot_out, unsigned long long *
 
 // payload rows of the re-classified representatives -> their slots; a row
 // whose hash does not reproduce the slot key flags an error
-__global__ void k_hist_payload(HistDev H, const uint32_t *slots, const unsigned long long *idx, int64_t n,
+// rows i*R .. i*R+R-1 belong to stale record i (R = runs replayed per record); the
+// first row reproducing the key is the representative's payload
+__global__ void k_hist_payload(HistDev H, const uint32_t *slots, const unsigned long long *idx, int64_t n, int R,
                                const uint32_t *hash, const uint8_t *w, const uint8_t *h, const uint16_t *cells,
                                const unsigned long long *shape, unsigned int *err) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = slots[i];
-    if (hash[i] != (uint32_t)H.keys[s]) { atomicOr(err, 1u); continue; }
-    H.whc[s] = (uint32_t)w[i] | ((uint32_t)h[i] << 8) | ((uint32_t)cells[i] << 16);
-    for (int j = 0; j < H.W; j++) H.shape[s * H.W + j] = shape[i * H.W + j];
+    const uint32_t key = (uint32_t)H.keys[s];
+    int64_t q = -1;
+    for (int j = 0; j < R && q < 0; j++)
+      if (hash[i * R + j] == key) q = i * R + j;
+    if (q < 0) { atomicOr(err, 1u); continue; }
+    H.whc[s] = (uint32_t)w[q] | ((uint32_t)h[q] << 8) | ((uint32_t)cells[q] << 16);
+    for (int j = 0; j < H.W; j++) H.shape[s * H.W + j] = shape[q * H.W + j];
     H.pay_idx[s] = idx[i];
   }
 }

@@ -28,10 +28,12 @@ struct ClassifyParams {
   // histogram mode (enumerate_range): no per-genome outputs
   int32_t hist_mode;
   HistDev hist;
-  // payload mode (histogram export, fast kernel): replay runs of item i until one
-  // ends BOUNDED with hash pay_key[i]; write its hash/w/h/cells/shape row and stop
-  // (no such run: out_hash[i] = ~pay_key[i])
+  // payload mode (histogram export, fast kernel), R = 2^pay_shift runs per record:
+  // item i replays run i % R of record i / R (all runs in parallel lanes); if it ends
+  // BOUNDED with hash pay_key[i / R] it writes its hash/w/h/cells/shape row i, else
+  // out_hash[i] = ~pay_key[i / R].  The caller takes each record's first matching run.
   int32_t pay_mode;
+  int32_t pay_shift;
   const uint32_t *pay_key;
   // GA fitness mode (JaTAM-shape fitness): out_fit[i] =
   // d^2 - shapediff(target, run-0 grid) for genomes DET at hist_k, else 0.
