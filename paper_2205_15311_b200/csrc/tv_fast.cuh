@@ -79,22 +79,27 @@ template <typename M, int NC, bool STRICT> struct CandSwar {
 
   __device__ __forceinline__ static uint32_t partner(uint32_t e) { return e ? (((e - 1u) ^ 1u) + 1u) : 15u; }
 
-  // face labels and partners of every candidate (E, P); build() adds the rest
+  // face labels and partners of every candidate (E, P); build() adds the rest.
+  // Candidate (t, r) shows lab[4t + ((k - r) & 3)] on side k, so tile t's 16-bit chunk of
+  // E3 is its labels nibble-reversed (rev = L3 L2 L1 L0, nibble 0 first) and E0 / E1 / E2
+  // are rev rotated left by 1 / 2 / 3 nibbles.  Partners ((e - 1) ^ 1) + 1, 0 -> 15, in SWAR
+  // (labels <= 7 on this path: no borrow or carry crosses a nibble).
   __device__ __forceinline__ void build_faces(const uint32_t *lab) {
-    E0 = E1 = E2 = E3 = P0 = P1 = P2 = P3 = 0;
+    E0 = E1 = E2 = E3 = 0;
 #pragma unroll
     for (int t = 0; t < NC / 4; t++) {
-#pragma unroll
-      for (int r = 0; r < 4; r++) {
-        const int c = t * 4 + r;
-        const uint32_t e0 = lab[t * 4 + ((0 - r) & 3)], e1 = lab[t * 4 + ((1 - r) & 3)];
-        const uint32_t e2 = lab[t * 4 + ((2 - r) & 3)], e3 = lab[t * 4 + ((3 - r) & 3)];
-        E0 |= (M)e0 << (4 * c); E1 |= (M)e1 << (4 * c);
-        E2 |= (M)e2 << (4 * c); E3 |= (M)e3 << (4 * c);
-        P0 |= (M)partner(e0) << (4 * c); P1 |= (M)partner(e1) << (4 * c);
-        P2 |= (M)partner(e2) << (4 * c); P3 |= (M)partner(e3) << (4 * c);
-      }
+      const uint32_t rev = lab[4 * t + 3] | (lab[4 * t + 2] << 4) | (lab[4 * t + 1] << 8) | (lab[4 * t] << 12);
+      const uint32_t dup = rev | (rev << 16);
+      E0 |= (M)((dup >> 12) & 0xFFFFu) << (16 * t); E1 |= (M)((dup >> 8) & 0xFFFFu) << (16 * t);
+      E2 |= (M)((dup >> 4) & 0xFFFFu) << (16 * t); E3 |= (M)rev << (16 * t);
     }
+    P0 = partners(E0); P1 = partners(E1); P2 = partners(E2); P3 = partners(E3);
+  }
+  __device__ __forceinline__ static M partners(M x) {
+    constexpr M ONES = VALID >> 3;                   // 0x11..1 over the NC candidate nibbles
+    const M z = (~nz_nib<M>(x) & VALID) >> 3;        // 1 in every zero nibble
+    const M x1 = x | z;                              // zero nibbles -> 1 (no borrow below)
+    return ((((x1 - ONES) ^ ONES) + ONES) | (z * (M)15));
   }
 
   __device__ __forceinline__ void build(const uint32_t *lab, int ntiles) {
