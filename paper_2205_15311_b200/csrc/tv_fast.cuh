@@ -104,26 +104,40 @@ template <typename M, int NC, bool STRICT> struct CandSwar {
 
   __device__ __forceinline__ void build(const uint32_t *lab, int ntiles) {
     build_faces(lab);
-    uint32_t code[NC];
+    // equivalence-class id = lowest candidate with the same in-situ code (_k:199).  Candidate
+    // (t, r) has code rotl16(X_t, 4r), X_t = L0 | L1 << 4 | L2 << 8 | L3 << 12, so inside a tile
+    // the ids repeat with the tile's rotational period, and tile t2's rotations map onto those
+    // of the first earlier tile t1 with X_t2 = rotl16(X_t1, 4s): code(t2, r) = code(t1, r + s).
+    constexpr int T = NC / 4;
+    uint32_t X[T], id[NC];
 #pragma unroll
-    for (int t = 0; t < NC / 4; t++) {
+    for (int t = 0; t < T; t++) {
+      X[t] = lab[4 * t] | (lab[4 * t + 1] << 4) | (lab[4 * t + 2] << 8) | (lab[4 * t + 3] << 12);
+      const uint32_t dup = X[t] | (X[t] << 16);
+      const uint32_t m = t >= ntiles ? 3u  // absent tiles: unique ids, never equal to anything
+                         : ((dup >> 12) & 0xFFFFu) == X[t] ? 0u : ((dup >> 8) & 0xFFFFu) == X[t] ? 1u : 3u;
 #pragma unroll
-      for (int r = 0; r < 4; r++) {
-        const int c = t * 4 + r;
-        code[c] = t < ntiles ? (get_nib<M>(E0, c) | (get_nib<M>(E1, c) << 4) | (get_nib<M>(E2, c) << 8) |
-                                (get_nib<M>(E3, c) << 12))
-                             : 0xFFFF0000u | (uint32_t)c;
+      for (int r = 0; r < 4; r++) id[4 * t + r] = (uint32_t)(4 * t) + ((uint32_t)r & m);
+    }
+#pragma unroll
+    for (int t2 = 1; t2 < T; t2++) {
+      bool matched = t2 >= ntiles;
+#pragma unroll
+      for (int t1 = 0; t1 < t2; t1++) {
+        const uint32_t dup = X[t1] | (X[t1] << 16);
+#pragma unroll
+        for (int sft = 0; sft < 4; sft++) {
+          const uint32_t rot = sft ? (dup >> (16 - 4 * sft)) & 0xFFFFu : X[t1];
+          const bool hit = !matched && rot == X[t2];
+#pragma unroll
+          for (int r = 0; r < 4; r++) id[4 * t2 + r] = hit ? id[4 * t1 + ((r + sft) & 3)] : id[4 * t2 + r];
+          matched = matched || hit;
+        }
       }
     }
     CLS = 0;
 #pragma unroll
-    for (int c = 0; c < NC; c++) {
-      uint32_t id = (uint32_t)c;
-#pragma unroll
-      for (int c2 = NC - 1; c2 >= 0; c2--)
-        if (c2 < c && code[c2] == code[c]) id = (uint32_t)c2;
-      CLS |= (M)id << (4 * c);
-    }
+    for (int c = 0; c < NC; c++) CLS |= (M)id[c] << (4 * c);
     N0 = nz_nib<M>(E0) & VALID; N1 = nz_nib<M>(E1) & VALID;
     N2 = nz_nib<M>(E2) & VALID; N3 = nz_nib<M>(E3) & VALID;
   }
