@@ -129,6 +129,7 @@ int build_decoder(int a, int bpl, const int64_t *mask_pos, const uint8_t *mask_v
     D.nf[te] = (uint8_t)nf;
     D.lo[te] = (uint8_t)(lo < 0 ? 0 : lo);
     D.sh[te] = (uint8_t)(sh < 0 ? 0 : sh);
+    D.pk[te] = (uint32_t)D.lo[te] | (((1u << nf) - 1u) << 8) | ((uint32_t)D.sh[te] << 16) | ((uint32_t)fix << 24);
     if (!contiguous) general = true;
   }
   D.general = general ? 1 : 0;

@@ -78,15 +78,17 @@ struct LabelDecoder {
   int32_t general;  // 0: fast form for every label
   int32_t pad_;
   uint8_t lo[64], nf[64], sh[64], fix[64];
+  uint32_t pk[64];  // fast form packed: lo | ((1 << nf) - 1) << 8 | sh << 16 | fix << 24
   uint8_t src[64 * 8];
 };
 
 __device__ __forceinline__ uint32_t decode_label(const LabelDecoder &D, int te, uint64_t idx) {
+  if (!D.general) {  // one constant load, no branch
+    const uint32_t w = D.pk[te];
+    return (w >> 24) | (((uint32_t)(idx >> (w & 63u)) & ((w >> 8) & 0xFFu)) << ((w >> 16) & 0xFFu));
+  }
   uint32_t v = D.fix[te];
-  if (!D.general) {
-    const uint32_t nf = D.nf[te];
-    if (nf) v |= ((uint32_t)(idx >> D.lo[te]) & ((1u << nf) - 1u)) << D.sh[te];
-  } else {
+  {
     for (int k = 0; k < D.bpl; k++) {
       const uint32_t s = D.src[te * 8 + k];
       if (s != 0xFF) v |= (uint32_t)((idx >> s) & 1ULL) << k;

@@ -531,14 +531,21 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
           } else {
             // behaviour-sorted processing order (k_prepass); every per-item output and flag below
             // is addressed by the item's own number, so the order is invisible to the caller
-            if (P.order) item = (int64_t)P.order[item];
+            bool tf = false;  // trivial-freedom bit (k_prepass): bit 31 of the order entry or a flag
+            if (P.order) {
+              const uint32_t o = P.order[item];
+              item = (int64_t)(o & 0x7FFFFFFFu);
+              tf = (o >> 31) != 0u;
+            } else if (P.tf_flags) {
+              tf = ((P.tf_flags[item >> 5] >> (item & 31)) & 1u) != 0u;
+            }
             const int64_t rec = item >> P.pay_shift;  // payload mode: item = (record, run)
             idx = item_index(P.indices, P.start, P.chunk, P.stride, P.item0 + rec);
             uint32_t lab[12];  // decode labels (_k:384-401)
 #pragma unroll
             for (int te = 0; te < 12; te++) lab[te] = te < NC ? decode_label(P.dec, te, idx) : 0u;
             K.build(lab, A);
-            tfree = P.tf_flags ? ((P.tf_flags[item >> 5] >> (item & 31)) & 1u) != 0u : false;
+            tfree = tf;
             trivial_at = first_unbound = first_mismatch = -1;
             run = (int)item & ((1 << P.pay_shift) - 1);
             replay = 0;
@@ -726,7 +733,7 @@ __global__ void __launch_bounds__(256, TV_PREPASS_MINB) k_prepass(const __grid_c
                       ((selfr ? 0u : 1u) << 4) | (uint32_t)(8 - nbr);
         kk = (kk << 1) | (f ? 0u : 1u);  // trivial-freedom (a <= 2) as the lowest key bit
         key_out[item] = (uint16_t)kk;
-        iota_out[item] = (uint32_t)item;
+        iota_out[item] = (uint32_t)item | (f ? 0x80000000u : 0u);  // items < 2^31; bit 31 = flag
       }
     }
     if (flags) {
