@@ -44,7 +44,7 @@ __device__ __forceinline__ int ffs_m(uint64_t x) { return __ffsll((long long)x) 
 
 struct FastLane {
   uint32_t *gw;     // &board word 0 of this lane (stride 32 words)
-  uint32_t *sw;     // &stack word 0 of this lane (stride 32 words, 2 entries per word)
+  uint16_t *sw;     // &stack entry 0 of this lane: entry j at sw[j * 32] (lanes 2k, 2k+1 share a bank word)
   uint16_t *spill;  // &spill entry 0 of this lane (stride 32)
   int S;
   __device__ __forceinline__ uint32_t nib(int lin) const {
@@ -56,11 +56,11 @@ struct FastLane {
     *p = (*p & ~(15u << s)) | (v << s);
   }
   __device__ __forceinline__ uint32_t st_read(int j) const {
-    if (j < S) return reinterpret_cast<const uint16_t *>(sw + (j >> 1) * 32)[j & 1];
+    if (j < S) return sw[j * 32];
     return spill[(int64_t)(j - S) * 32];
   }
   __device__ __forceinline__ void st_write(int j, uint32_t e) const {
-    if (j < S) reinterpret_cast<uint16_t *>(sw + (j >> 1) * 32)[j & 1] = (uint16_t)e;
+    if (j < S) sw[j * 32] = (uint16_t)e;
     else spill[(int64_t)(j - S) * 32] = (uint16_t)e;
   }
 };
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
   const int words_per_warp = (P.GW + P.S / 2) * 32;
   FastLane Ln;
   Ln.gw = smem + warp * words_per_warp + lane;
-  Ln.sw = Ln.gw + P.GW * 32;
+  Ln.sw = reinterpret_cast<uint16_t *>(smem + warp * words_per_warp + P.GW * 32) + lane;
   Ln.S = P.S;
   const int64_t gwarp = (int64_t)blockIdx.x * nwarps + warp;
   Ln.spill = P.spill + gwarp * (int64_t)P.spill_cap * 32 + lane;

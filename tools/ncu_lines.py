@@ -1,12 +1,13 @@
 """Aggregate an ncu report's SASS metrics per CUDA source line.
 
-usage: python tools/ncu_lines.py report.ncu-rep [top]
+usage: python tools/ncu_lines.py report.ncu-rep [top] [kernel-regex]
 """
 import csv, io, subprocess, sys, collections
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
+kf = ["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+txt = subprocess.run(["ncu", "-i", rep, *kf, "--page", "source", "--csv", "--print-source=cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(txt)))
 agg = collections.defaultdict(lambda: [0.0, 0.0, 0.0, ""])
