@@ -930,7 +930,7 @@ int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **
   if (per_sm < 1) { delete h; return fail(TV_ERR_CUDA, "GA kernel does not fit one CTA per SM"); }
   h->nblocks = nsm;
   if (const char *ec = getenv("TV_GA_CTAS")) h->nblocks = std::max(1, std::min(nsm, atoi(ec)));  // A/B only
-  P.chunk = (n + h->nblocks - 1) / h->nblocks;
+  P.chunk = ((n + h->nblocks - 1) / h->nblocks + 31) / 32 * 32;  // whole rows of 32 (k_ga_run)
   h->device = dev;
   h->cur = 0;
   cudaError_t e = cudaSuccess;
@@ -940,6 +940,7 @@ int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **
   e = e ? e : cudaMalloc(&P.guide, (size_t)n * sizeof(ulonglong2));
   e = e ? e : cudaMalloc(&P.fstage, n * 4);
   e = e ? e : cudaMalloc(&P.tot, (size_t)h->nblocks * 8);
+  e = e ? e : cudaMalloc(&P.rowx, (size_t)h->nblocks * (size_t)(P.chunk / 32) * 4);
   e = e ? e : cudaMalloc(&P.done, 8);
   e = e ? e : cudaMalloc(&P.final_buf, 4);
   e = e ? e : cudaMemset(P.pop0, 0, n * 8);
@@ -952,6 +953,7 @@ int tv_ga_destroy(tv_ga *h) {
   if (!h) return 0;
   GaParams &P = h->P;
   cudaFree(P.pop0); cudaFree(P.pop1); cudaFree(P.cdf); cudaFree(P.guide); cudaFree(P.fstage); cudaFree(P.tot);
+  cudaFree(P.rowx);
   cudaFree(P.done); cudaFree(P.final_buf);
   delete h;
   return 0;

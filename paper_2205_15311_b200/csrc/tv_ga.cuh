@@ -55,6 +55,7 @@ struct GaParams {
   ulonglong2 *guide;     // n buckets (first B used per generation): x = (cdf[j] << 32) | j,
                          // y = genome j (packed mode, L <= 32)
   unsigned long long *tot;  // per CTA chunk totals
+  uint32_t *rowx;        // per CTA, per row of 32 individuals: fitness sum, then its exclusive offset
   uint32_t *best;        // n_gens
   unsigned long long *sum;  // n_gens
   uint32_t *count;       // n_gens
@@ -149,74 +150,103 @@ __device__ __forceinline__ uint64_t ga_pick_genome(const GaParams &P, const unsi
   return g;
 }
 
+// Block-wide exclusive scan of this CTA's row sums (rowx[0..nrows), in place) and the
+// stats of the population they describe; returns the CTA total (all threads).
+__device__ __forceinline__ uint32_t ga_rows_scan(uint32_t *rowx, int nrows, uint32_t *warp_sum, uint32_t *s_carry) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) *s_carry = 0u;
+  __syncthreads();
+  for (int r0 = 0; r0 < nrows; r0 += nt) {
+    const int r = r0 + tid;
+    const uint32_t v = r < nrows ? rowx[r] : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      const uint32_t w0 = lane < (nt >> 5) ? warp_sum[lane] : 0u;
+      uint32_t w = w0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, w, o);
+        if (lane >= o) w += y;
+      }
+      warp_sum[lane] = w - w0;
+      if (lane == 31) warp_sum[32] = w;  // this tile's total
+    }
+    __syncthreads();
+    const uint32_t carry = *s_carry;
+    if (r < nrows) rowx[r] = carry + warp_sum[wid] + x - v;
+    __syncthreads();
+    if (tid == 0) *s_carry = carry + warp_sum[32];
+    __syncthreads();
+  }
+  return *s_carry;
+}
+
+// One cooperative launch runs n_gens generations.  Per generation two grid barriers:
+//   B: the CTA chunk offsets -> global inclusive CDF (packed above the genome for L <= 32)
+//      and the guide table, from per-row exclusive offsets scanned at the end of the
+//      previous phase C; stop decision.
+//   C: children (TV_GA_ILP per thread in flight); each warp makes one row of 32
+//      consecutive children at a time, so the row's fitness sum, best and count for the
+//      next generation come from warp reductions, and a block scan of the row sums
+//      replaces a separate pass over the staged fitness.
 __global__ void __launch_bounds__(1024, 1) k_ga_run(const __grid_constant__ GaParams P) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
-  __shared__ uint32_t warp_sum[32];  // blockDim.x == 1024
-  __shared__ uint32_t s_best, s_cnt;
+  __shared__ uint32_t warp_sum[33];  // blockDim.x == 1024
+  __shared__ uint32_t s_best, s_cnt, s_carry;
   __shared__ unsigned long long s_off, s_total;
   __shared__ int s_stop;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
-  const int64_t c0 = (int64_t)blockIdx.x * P.chunk;
+  const int64_t c0 = (int64_t)blockIdx.x * P.chunk;  // P.chunk is a multiple of 32
   const int64_t c1 = min(P.n, c0 + P.chunk);
   const int64_t len = max((int64_t)0, c1 - c0);
-  // phases A/B: warp w owns the contiguous segment [c0 + w*seg, c0 + (w+1)*seg)
-  // walked in rows of 32 consecutive individuals (coalesced loads and stores)
-  const int64_t seg = ((len + nt - 1) / nt) * 32;  // (rows per warp) x 32
-  const int64_t s0 = c0 + (int64_t)wid * seg;
-  const int rows = (int)(seg >> 5);
+  const int nrows = (int)((len + 31) >> 5);
+  uint32_t *rowx = P.rowx + (int64_t)blockIdx.x * (P.chunk >> 5);
   int cur = 0;
   int64_t t = 0;
-  // fitness of the initial population, staged in index order
   const uint64_t full = P.L == 64 ? ~0ULL : ((1ULL << P.L) - 1);
   const bool packed = P.L <= 32;
-  for (int64_t i = c0 + tid; i < c1; i += nt)
-    P.fstage[i] = P.fitness == 0 ? (uint32_t)__popcll(P.pop0[i] & full) : P.f_ext[i];
+  // fitness of the initial population, staged in index order, with its row sums and stats
   if (tid == 0) { s_best = 0; s_cnt = 0; }
   __syncthreads();
+  for (int r = wid; r < nrows; r += nt >> 5) {
+    const int64_t i = c0 + (int64_t)r * 32 + lane;
+    uint32_t f = 0;
+    if (i < c1) {
+      f = P.fitness == 0 ? (uint32_t)__popcll(P.pop0[i] & full) : P.f_ext[i];
+      P.fstage[i] = f;
+    }
+    const uint32_t s = __reduce_add_sync(0xFFFFFFFFu, f), mx = __reduce_max_sync(0xFFFFFFFFu, f);
+    const uint32_t nc = (uint32_t)__popc(__ballot_sync(0xFFFFFFFFu, f >= P.target && i < c1));
+    if (lane == 0) {
+      rowx[r] = s;
+      atomicMax(&s_best, mx);
+      if (nc) atomicAdd(&s_cnt, nc);
+    }
+  }
+  __syncthreads();
+  {
+    const uint32_t tot = ga_rows_scan(rowx, nrows, warp_sum, &s_carry);
+    if (tid == 0) {
+      P.tot[blockIdx.x] = tot;
+      if (P.n_gens > 0) { atomicMax(&P.best[0], s_best); atomicAdd(&P.count[0], s_cnt); }
+      s_best = 0; s_cnt = 0;
+    }
+  }
+  grid.sync();
   for (; t < P.n_gens; t++) {
     const int64_t g = P.g0 + t;
     unsigned long long *pop = cur ? P.pop1 : P.pop0;
     unsigned long long *nxt = cur ? P.pop0 : P.pop1;
     const bool prof = P.prof && blockIdx.x == 0 && tid == 0;
     unsigned long long tp0 = prof ? ga_clock() : 0ull, tp1 = 0ull;
-    // ---- A: warp sums over its segment, block scan of warp totals, stats
-    uint32_t acc = 0, best = 0, cnt = 0;
-    for (int k = 0; k < rows; k++) {
-      const int64_t i = s0 + k * 32 + lane;
-      const uint32_t f = i < c1 ? P.fstage[i] : 0u;
-      acc += f;
-      best = max(best, f);
-      cnt += f >= P.target;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
-      best = max(best, __shfl_xor_sync(0xFFFFFFFFu, best, o));
-      cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
-    }
-    if (lane == 0) { warp_sum[wid] = acc; atomicMax(&s_best, best); atomicAdd(&s_cnt, cnt); }
-    __syncthreads();
-    if (wid == 0) {
-      const uint32_t v = lane < (nt >> 5) ? warp_sum[lane] : 0u;
-      uint32_t w = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, w, o);
-        if (lane >= o) w += y;
-      }
-      warp_sum[lane] = w - v;  // exclusive warp offsets
-      if (lane == 31) {
-        P.tot[blockIdx.x] = w;
-        atomicMax(&P.best[t], s_best);
-        atomicAdd(&P.count[t], s_cnt);
-      }
-    }
-    __syncthreads();
-    const uint32_t excl = warp_sum[wid];
-    if (tid == 0) { s_best = 0; s_cnt = 0; }  // consumed above; next written after several barriers
-    grid.sync();
-    if (prof) { tp1 = ga_clock(); P.prof[0] += tp1 - tp0; tp0 = tp1; }
     // ---- B: chunk offsets -> global CDF + guide table; stop decision
     if (wid == 0) {
       unsigned long long o = 0, tt = 0;
@@ -246,22 +276,26 @@ __global__ void __launch_bounds__(1024, 1) k_ga_run(const __grid_constant__ GaPa
     if (blockIdx.x == 0 && tid == 0) P.sum[t] = s_total;
     if (s_stop) { t++; break; }
     {
-      uint32_t base = (uint32_t)s_off + excl;  // inclusive CDF before this warp's current row
-      constexpr int RB = 4;  // rows whose loads are issued before any store (stores could alias them)
-      for (int k0 = 0; k0 < rows; k0 += RB) {
-        uint32_t fr[RB];
+      const uint32_t off = (uint32_t)s_off;
+      constexpr int RB = 2;  // rows whose loads are issued before any store (stores could alias them; 4 spills)
+      const int wstep = nt >> 5;
+      for (int k0 = wid; k0 < nrows; k0 += RB * wstep) {
+        uint32_t fr[RB], bx[RB];
         uint64_t gr[RB];
 #pragma unroll
         for (int u = 0; u < RB; u++) {
-          const int64_t i = s0 + (k0 + u) * 32 + lane;
-          const bool in = k0 + u < rows && i < c1;
+          const int r = k0 + u * wstep;
+          const int64_t i = c0 + (int64_t)r * 32 + lane;
+          const bool in = r < nrows && i < c1;
           fr[u] = in ? P.fstage[i] : 0u;
           gr[u] = in && packed ? (pop[i] & 0xFFFFFFFFull) : 0ull;
+          bx[u] = r < nrows ? rowx[r] : 0u;
         }
 #pragma unroll
         for (int u = 0; u < RB; u++) {
-          if (k0 + u >= rows) break;
-          const int64_t i = s0 + (k0 + u) * 32 + lane;
+          const int r = k0 + u * wstep;
+          if (r >= nrows) break;
+          const int64_t i = c0 + (int64_t)r * 32 + lane;
           const uint32_t f = fr[u];
           uint32_t x = f;
 #pragma unroll
@@ -269,7 +303,7 @@ __global__ void __launch_bounds__(1024, 1) k_ga_run(const __grid_constant__ GaPa
             const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
             if (lane >= o) x += y;
           }
-          const uint32_t run = base + x, prev = run - f;
+          const uint32_t run = off + bx[u] + x, prev = run - f;
           if (i < c1) {
             if (packed) pop[i] = ((unsigned long long)run << 32) | gr[u];
             else P.cdf[i] = run;
@@ -280,17 +314,17 @@ __global__ void __launch_bounds__(1024, 1) k_ga_run(const __grid_constant__ GaPa
               for (int64_t b = b0; b <= b1; b++) P.guide[b] = e;
             }
           }
-          base = __shfl_sync(0xFFFFFFFFu, run, 31);
         }
       }
     }
     grid.sync();
     if (prof) { tp1 = ga_clock(); P.prof[1] += tp1 - tp0; tp0 = tp1; }
     const uint64_t gkey = mix64(P.seed ^ (kGold * ((uint64_t)g + 1)));  // stream_state prefix (_k:45-48)
-    // ---- C: children, TV_GA_ILP at a time (draws first, then the dependent loads);
-    //      the next generation's fitness is staged as the children are made
+    // ---- C: children, TV_GA_ILP at a time (draws first, then the dependent loads); warp w
+    //      makes rows w, w + 32, ... so row sums / best / count of the next generation are
+    //      warp reductions
     constexpr int NI = TV_GA_ILP;
-    for (int64_t i = c0 + tid; i < c1; i += NI * nt) {
+    for (int64_t i = c0 + tid; i < c0 + (int64_t)nrows * 32; i += NI * nt) {
       ChildDraws D[NI];
 #pragma unroll
       for (int u = 0; u < NI; u++) {
@@ -324,15 +358,40 @@ __global__ void __launch_bounds__(1024, 1) k_ga_run(const __grid_constant__ GaPa
 #pragma unroll
       for (int u = 0; u < NI; u++) {
         const int64_t iu = i + u * nt;
+        const int r = (int)((iu - c0) >> 5);
+        uint32_t f = 0;
         if (iu < c1) {
           const uint64_t c = (cv[u] ^ D[u].flips) & full;
           nxt[iu] = c;
-          if (P.fitness == 0) P.fstage[iu] = (uint32_t)__popcll(c);
+          if (P.fitness == 0) {
+            f = (uint32_t)__popcll(c);
+            P.fstage[iu] = f;
+          } else {
+            f = P.fstage[iu];  // external fitness stays that of the staged population
+          }
+        }
+        if (r < nrows) {  // warp-uniform: a warp's lanes make one row
+          const uint32_t s = __reduce_add_sync(0xFFFFFFFFu, f), mx = __reduce_max_sync(0xFFFFFFFFu, f);
+          const uint32_t nc = (uint32_t)__popc(__ballot_sync(0xFFFFFFFFu, f >= P.target && iu < c1));
+          if (lane == 0) {
+            rowx[r] = s;
+            atomicMax(&s_best, mx);
+            if (nc) atomicAdd(&s_cnt, nc);
+          }
         }
       }
     }
     cur ^= 1;
-    __syncthreads();  // this CTA's staged fitness is read in index order by phase A
+    __syncthreads();
+    {
+      const uint32_t tot = ga_rows_scan(rowx, nrows, warp_sum, &s_carry);
+      if (tid == 0) {
+        P.tot[blockIdx.x] = tot;
+        if (t + 1 < P.n_gens) { atomicMax(&P.best[t + 1], s_best); atomicAdd(&P.count[t + 1], s_cnt); }
+        s_best = 0; s_cnt = 0;
+      }
+    }
+    grid.sync();
     if (prof) P.prof[2] += ga_clock() - tp0;
   }
   if (blockIdx.x == 0 && tid == 0) {
