@@ -1,9 +1,6 @@
 // tv_ga.cuh -- GA generation loop (SPEC.md evolve module).
 //
 // One cooperative persistent kernel runs many generations; per generation:
-//   A. per-thread sums over a contiguous run of the fitness vector (staged in
-//      index order when the children were made), block scan, stats;
-//   -- grid barrier --
 //   B. chunk offsets -> global inclusive CDF (u32) and a guide table for
 //      indexed search (Chen & Asau): the r-range [0, total) is cut into
 //      B = min(n, total) monotone buckets b(r) = (r * M) >> 32 and guide[b] =
@@ -12,13 +9,18 @@
 //      the genome in the population word and the guide carries the genome, so
 //      most selections are a single L2 read); individual j writes the
 //      buckets whose first r lies in its own range [cdf[j-1], cdf[j]), so the
-//      table is built in the same pass;
+//      table is built in the same pass.  Rows of 32 individuals are
+//      independent: each starts at its exclusive offset from the last phase C;
 //   -- grid barrier --
 //   C. children: all random draws of a child first (selection draws,
 //      crossover mask, mutation mask), then selection = guide[b(r)] plus a short
 //      forward scan while cdf[j] <= r (exactly the first j with cdf[j] > r),
-//      parent loads and the child, two children interleaved per thread; the
-//      child's Fujiyama fitness is staged for the next generation's phase A.
+//      parent loads and the child, two children interleaved per thread; a warp
+//      makes one row of 32 consecutive children at a time, so the next
+//      generation's row fitness sums, best and target count are warp
+//      reductions; a block scan turns the row sums into row offsets and the
+//      CTA total (the prologue does the same for the initial population);
+//   -- grid barrier --
 // Two grid barriers per generation.
 // Data written by other CTAs is read only after a grid barrier (grid.sync()
 // orders and publishes all prior writes of the grid; its gpu-scope acquire
