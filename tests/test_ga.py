@@ -207,6 +207,23 @@ def test_jatam_fitness_matches_cpu():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("n", [100, 1000 + 7, 148 * 32 + 5])
+def test_device_ga_target_zero_counts_every_individual(n):
+    """count_at_target with target 0 is the population size: padding lanes of partial rows and
+    empty CTAs (population not a multiple of 32 per CTA) must not be counted."""
+    L, lam = 24, 0.5
+    ga = E.DeviceGA(n, L, lam, "asexual")
+    ga.set_population(np.zeros(n, np.uint64))
+    k, b, s, c = ga.run(5, 0, 12, 0, n + 1, 0)
+    pop = np.zeros(n, np.uint64)
+    k2, b2, s2, c2 = O.ga_run(pop, L, 0, E.poisson_thresholds(lam, L), 5, 0, 12, 0, n + 1, 0)
+    assert k == k2 == 12 and np.all(np.asarray(c) == n)
+    assert np.array_equal(b, b2) and np.array_equal(s, s2) and np.array_equal(c, c2)
+    assert np.array_equal(ga.population(), pop)
+    ga.close()
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("n,L,mode,mu,stop", [(512, 32, "asexual", 0.3, "adaptation"), (777, 24, "single_point", 1.0, "never"),
                                                (4096, 64, "uniform", 0.1, "discovery"), (512, 32, "asexual", 4.0, "adaptation")])
 def test_replicas_equal_single_runs(n, L, mode, mu, stop):
