@@ -46,6 +46,15 @@ N_S28 = 1 << 24
 CHUNK = 1 << 20
 
 
+def max_over_ranks(x: float) -> float:
+    """Max of a host float over all ranks (device tensor on NCCL, host tensor otherwise)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def env_int(name, default):
     try:
         return int(os.environ.get(name, default))
@@ -266,9 +275,7 @@ def s32_bench(args, rank: int, world: int, stream) -> dict:
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms)
     final = merged if merged is not None else hist.export(sp)
     hist.close()
     try:
@@ -386,10 +393,17 @@ def main():
 
     import torch
     import torch.distributed as dist
+    # TV_DIST_BACKEND=gloo runs the multi-rank path with several ranks on one GPU (tests only)
+    backend = os.environ.get("TV_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend, rank=rank, world_size=world)
     from paper_2205_15311_b200 import _lib
     from paper_2205_15311_b200.classify import DeviceHistogram, enumerate_space, shape_words_for
     from paper_2205_15311_b200.distributed import allreduce_device_histogram, enumerate_space_distributed
@@ -448,9 +462,7 @@ def main():
     kern_ms = [e1.elapsed_time(e2) for _, e1, e2 in ev] if world == 1 else None
     total_ms = sum(step_ms)
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = max_over_ranks(total_ms)
     ms_per_step = total_ms / args.steps
     value = N_S28 / (ms_per_step / 1e3)
 
@@ -474,9 +486,7 @@ def main():
         d2h = len(h) * (4 + 8 * 4 + 1 + 1 + 2 + 8 * W) + h.tallies.size * 8
     e2e_s = statistics.median(e2e_times)
     if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s = max_over_ranks(e2e_s)
     h2d = ks.nbytes + mp.nbytes + mv.nbytes + fp.nbytes
 
     # ---- roofline: dominant kernel vs measured int32 ALU peak

@@ -107,16 +107,20 @@ def allreduce_device_histogram(dev: DeviceHistogram, group=None, meta: dict | No
     world = dist.get_world_size(group)
     n_local, _ = dev.count()
     dv = torch.device("cuda", torch.cuda.current_device())
-    nmax = torch.tensor([n_local], dtype=torch.int64, device=dv)
+    # collectives on the device for NCCL; other backends (gloo: several ranks sharing one GPU
+    # in tests) move the same tensors through host memory
+    cv = dv if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    nmax = torch.tensor([n_local], dtype=torch.int64, device=cv)
     dist.all_reduce(nmax, op=dist.ReduceOp.MAX, group=group)
     nmax = max(1, int(nmax.item()))
     rows = torch.zeros((nmax, dev.row_width), dtype=torch.int64, device=dv)
     tallies = torch.zeros((len(dev.ks), 5), dtype=torch.int64, device=dv)
     dev.pack_into(rows, tallies)
-    allrows = torch.empty((world * nmax, dev.row_width), dtype=torch.int64, device=dv)
-    dist.all_gather_into_tensor(allrows, rows, group=group)
-    dist.all_reduce(tallies, op=dist.ReduceOp.SUM, group=group)
-    dev.replace_rows(allrows, tallies)
+    allrows = torch.empty((world * nmax, dev.row_width), dtype=torch.int64, device=cv)
+    rows_c, tallies_c = rows.to(cv), tallies.to(cv)
+    dist.all_gather_into_tensor(allrows, rows_c, group=group)
+    dist.all_reduce(tallies_c, op=dist.ReduceOp.SUM, group=group)
+    dev.replace_rows(allrows.to(dv), tallies_c.to(dv))
     return dev.export(meta=meta)
 
 
