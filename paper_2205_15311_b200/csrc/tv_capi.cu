@@ -157,8 +157,7 @@ int fill_common(int32_t a, int32_t bpl, const int64_t *mask_pos, const uint8_t *
   if (hist_k < 1 || hist_k > kmax) return fail(TV_ERR_ARG, "hist_k=%d outside [1, ks[-1]=%d]", hist_k, kmax);
   C.P.a = a; C.P.d = d; C.P.strict = strict ? 1 : 0; C.P.q = (int32_t)q; C.P.kmax = kmax; C.P.hist_k = hist_k;
   C.P.seed = seed;
-  const int PD = d + 2;
-  C.fast = a <= 3 && bpl <= 3 && PD * ((PD + 7) / 8) * 8 < 65536 && PD < 256;  // cell ids fit u16
+  C.fast = a <= 3 && bpl <= 3 && d <= 118;  // row stride < 128 (byte cell offsets, tv_fast.cuh)
   return 0;
 }
 

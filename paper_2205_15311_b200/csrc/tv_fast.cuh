@@ -617,13 +617,13 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
     }
     minr = min(minr, r); maxr = max(maxr, r);                                 // _k:217-224
     minc = min(minc, c); maxc = max(maxc, c);
-    // new frontier N,E,S,W (_k:225-237) as 2-bit direction codes, one per byte
+    // new frontier N,E,S,W (_k:225-237) as cell offsets + 128, one per byte (RS < 128)
     uint32_t nbp = 0;
     int m = 0;
-    if (vN == 0x3Cu) { nbp |= 0u << (8 * m); m++; }
-    if (vE == 0x3Cu) { nbp |= 1u << (8 * m); m++; }
-    if (vS == 0x3Cu) { nbp |= 2u << (8 * m); m++; }
-    if (vW == 0x3Cu) { nbp |= 3u << (8 * m); m++; }
+    if (vN == 0x3Cu) { nbp |= (uint32_t)(128 - RS) << (8 * m); m++; }
+    if (vE == 0x3Cu) { nbp |= 129u << (8 * m); m++; }
+    if (vS == 0x3Cu) { nbp |= (uint32_t)(128 + RS) << (8 * m); m++; }
+    if (vW == 0x3Cu) { nbp |= 127u << (8 * m); m++; }
     if (m >= 2) {  // Fisher-Yates (_k:238-242): both draws of m == 3 mixed side by side
       const bool three = m == 3;
       const uint32_t h1 = rng_hi(rs + kGold), h2 = rng_hi(rs + 2 * kGold);
@@ -639,9 +639,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
 #pragma unroll
     for (int j = 0; j < 3; j++) {
       if (j < mm) {
-        const uint32_t dir = (nbp >> (8 * j)) & 3u;
-        const int dl = (dir & 1u) ? 1 : RS;
-        const int nl = ((dir + 1u) & 2u) ? lin + dl : lin - dl;
+        const int nl = lin + (int)((nbp >> (8 * j)) & 0xFFu) - 128;
         Ln.st_write(sp + j, (uint32_t)nl);
         atomicAnd(&Ln.gw[(nl >> 3) * 32], ~(1u << ((nl & 7) * 4)));  // F -> E (one ATOMS, lane-private word)
       }
