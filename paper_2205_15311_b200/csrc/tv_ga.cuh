@@ -15,7 +15,7 @@
 //   C. children: all random draws of a child first (selection draws,
 //      crossover mask, mutation mask), then selection = guide[b(r)] plus a short
 //      forward scan while cdf[j] <= r (exactly the first j with cdf[j] > r),
-//      parent loads and the child, two children interleaved per thread; a warp
+//      parent loads and the child (TV_GA_ILP children in flight per thread); a warp
 //      makes one row of 32 consecutive children at a time, so the next
 //      generation's row fitness sums, best and target count are warp
 //      reductions; a block scan turns the row sums into row offsets and the
@@ -33,7 +33,7 @@
 #include "tv_device.cuh"
 
 #ifndef TV_GA_ILP
-#define TV_GA_ILP 2  // children per thread in flight in phase C (4 and 8 measured slower)
+#define TV_GA_ILP 1  // children per thread in flight in phase C (2 and 3 measured 0.7-2 % slower, 4 and 8 more)
 #endif
 
 namespace tvb {
