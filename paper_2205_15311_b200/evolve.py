@@ -281,6 +281,35 @@ class JatamFitness:
     strict: bool = True
 
 
+# Device GA handles kept between run_ga calls (population buffers, CDF, guide table: ~50 MB at
+# 2^20), like a caching allocator: cudaMalloc / cudaFree of these buffers costs 2-40 ms per call.
+_GA_POOL: "collections.OrderedDict" = None
+_GA_POOL_MAX = 4
+
+
+def _ga_acquire(n: int, L: int, mu_L: float, mode) -> "DeviceGA":
+    import collections
+    global _GA_POOL
+    if _GA_POOL is None:
+        _GA_POOL = collections.OrderedDict()
+    key = (int(n), int(L), float(mu_L), mode)
+    ga = _GA_POOL.pop(key, None)
+    if ga is None or not ga._h:
+        return DeviceGA(n, L, mu_L, mode)
+    ga.set_population(None)  # all-zero initial population, exactly as a fresh handle
+    return ga
+
+
+def _ga_release(ga: "DeviceGA", mu_L: float, mode) -> None:
+    key = (ga.n, ga.L, float(mu_L), mode)
+    old = _GA_POOL.pop(key, None)
+    if old is not None:
+        old.close()
+    _GA_POOL[key] = ga
+    while len(_GA_POOL) > _GA_POOL_MAX:
+        _GA_POOL.popitem(last=False)[1].close()
+
+
 def run_ga(cfg: GAConfig, fitness="fujiyama", seed: int = 0, chunk: int = 4096) -> RunRecord:
     """Generation loop on the device: evaluate, record, stop when the
     configured target is met (or at the cutoff), reproduce with full replacement."""
@@ -289,7 +318,8 @@ def run_ga(cfg: GAConfig, fitness="fujiyama", seed: int = 0, chunk: int = 4096) 
         raise ValueError("fitness must be 'fujiyama' or a JatamFitness")
     if jatam and fitness.space.free_bit_count != cfg.length:
         raise ValueError("GA genome length must equal the space's free bit count")
-    ga = DeviceGA(cfg.pop_size, cfg.length, cfg.mu_L, cfg.mode)
+    ga = _ga_acquire(cfg.pop_size, cfg.length, cfg.mu_L, cfg.mode)
+    ok = False
     try:
         if cfg.init is not None:
             ga.set_population(cfg.init)
@@ -308,8 +338,12 @@ def run_ga(cfg: GAConfig, fitness="fujiyama", seed: int = 0, chunk: int = 4096) 
             g += k
             if stop and c.size and ((stop == 1 and c[-1] >= 1) or (stop == 2 and c[-1] >= adapt_count)):
                 break
+        ok = True
     finally:
-        ga.close()
+        if ok:
+            _ga_release(ga, cfg.mu_L, cfg.mode)
+        else:
+            ga.close()
     best = np.concatenate(bests) if bests else np.zeros(0, np.uint32)
     cnt = np.concatenate(cnts) if cnts else np.zeros(0, np.uint32)
     mean = (np.concatenate(sums).astype(np.float64) / cfg.pop_size) if sums else np.zeros(0)
