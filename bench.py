@@ -7,8 +7,9 @@ all in the sm_100a bitboard kernel.  With N ranks the index range is dealt out
 in round-robin chunks (strong scaling: the job is always the whole space) and
 the per-rank histograms are combined with one device-resident NCCL exchange
 (paper_2205_15311_b200.distributed.allreduce_device_histogram: raw rows packed on
-the GPU, one all_gather + one all_reduce over NVLink, merge on the GPU, export)
-inside the step.
+the GPU, one all_gather + one all_reduce over NVLink, merge on the GPU) inside the
+step; at every N the step ends with the whole-space histogram resident on the GPU
+(the host export is part of e2e).
 
   value : device-timed (CUDA events, max over ranks) genomes/s, no host I/O.
   e2e   : the same job through the public API classify.enumerate_space (host
@@ -274,13 +275,14 @@ def s32_bench(args, rank: int, world: int, stream) -> dict:
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     run(mine * chunk)
-    merged = allreduce_device_histogram(hist, None) if world > 1 else None
+    if world > 1:  # the merged histogram stays on every GPU, as the 1-GPU one does
+        allreduce_device_histogram(hist, None, export=False)
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     if world > 1:
         ms = max_over_ranks(ms)
-    final = merged if merged is not None else hist.export(sp)
+    final = hist.export(sp)
     hist.close()
     try:
         gold = json.load(open(os.path.join(ROOT, "tests", "golden", "hist_s32_full.json")))
@@ -442,7 +444,7 @@ def main():
     for _ in range(args.warmup):
         enumerate_step()
         if world > 1:
-            allreduce_device_histogram(hist, None)
+            allreduce_device_histogram(hist, None, export=False)
     barrier()
     # ---- timed region: K steps, L2 flushed between steps (outside the events)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
@@ -458,7 +460,8 @@ def main():
             _lib.check(L.tv_enumerate_chunks(rank * CHUNK, count, CHUNK, CHUNK * world, a, bpl, _lib.ptr(mp),
                                              _lib.ptr(mv), mp.shape[0], _lib.ptr(fp), fp.shape[0], 19, _lib.ptr(ks),
                                              ks.shape[0], 8, 0, 1, hist._h, sp))
-            merged = allreduce_device_histogram(hist, None) if world > 1 else None
+            if world > 1:  # timed region ends, at every N, with the merged histogram on the GPU
+                allreduce_device_histogram(hist, None, export=False)
             e2.record(stream)
         barrier()
     info = _lib.launch_info()
@@ -471,7 +474,7 @@ def main():
     value = N_S28 / (ms_per_step / 1e3)
 
     # correctness of what was timed: the exported histogram equals the reference aggregate
-    final = hist.export(sp) if world == 1 else merged
+    final = hist.export(sp)
     tallies_ok = final.tallies.tolist() == [[7448198, 5894957, 0, 3434061, 0], [6939346, 6865723, 214055, 2758092, 0],
                                             [6697803, 7791627, 223880, 2063906, 0], [6631160, 8336639, 199388, 1610029, 0]]
 

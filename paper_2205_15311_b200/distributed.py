@@ -96,12 +96,14 @@ def allreduce_histogram(h: Histogram, group=None) -> Histogram:
     return out
 
 
-def allreduce_device_histogram(dev: DeviceHistogram, group=None, meta: dict | None = None) -> Histogram:
+def allreduce_device_histogram(dev: DeviceHistogram, group=None, meta: dict | None = None,
+                               export: bool = True) -> Histogram | None:
     """Device-resident exchange (NCCL): every rank packs its raw records on the GPU, one
     all_gather moves them over NVLink, one all_reduce sums the tallies, and each rank
     merges all rows into its own device histogram (tv_hist_replace_rows: counts added,
     representatives lowered, payload = lowest owner) before the export re-derives the
-    payloads whose owner is not the representative.  Same result as allreduce_histogram."""
+    payloads whose owner is not the representative.  Same result as allreduce_histogram.
+    export=False stops with the merged histogram resident in ``dev`` (returns None)."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
@@ -121,7 +123,7 @@ def allreduce_device_histogram(dev: DeviceHistogram, group=None, meta: dict | No
     dist.all_gather_into_tensor(allrows, rows_c, group=group)
     dist.all_reduce(tallies_c, op=dist.ReduceOp.SUM, group=group)
     dev.replace_rows(allrows.to(dv), tallies_c.to(dv))
-    return dev.export(meta=meta)
+    return dev.export(meta=meta) if export else None
 
 
 def rank_chunks(plan: list, rank: int, world: int) -> list:
