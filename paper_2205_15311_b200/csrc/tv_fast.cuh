@@ -236,7 +236,10 @@ template <typename M, int NC, bool STRICT> struct CandSwar {
         const uint32_t same = ~nz_nib<uint32_t>(pc[c1] ^ pc[c2]) & 0x8888u;  // same partner label per side
         const uint32_t b1 = bond[c1] & (STRICT ? (same | z[c2]) : 0x8888u);
         const uint32_t b2 = bond[c2] & (STRICT ? (same | z[c1]) : 0x8888u);
-        const bool pair = (bond[c1] & same) != 0u || (b1 && b2 && !(b1 == b2 && (b1 & (b1 - 1u)) == 0u));
+        // strict: b1 == b2 == one side k forces k into `same` (else both faces at k are 0 and
+        // neither bonds there), so the single-side exclusion only matters without the rule
+        const bool pair = (bond[c1] & same) != 0u ||
+                          (STRICT ? (b1 && b2) : (b1 && b2 && !(b1 == b2 && (b1 & (b1 - 1u)) == 0u)));
         ok = ok && !(pair && pc[c1] != pc[c2]);  // equal partner codes <=> equal in-situ codes
       }
     }
