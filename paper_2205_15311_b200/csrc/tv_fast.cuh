@@ -77,7 +77,6 @@ template <typename M, int NC, bool STRICT> struct CandSwar {
   M E0, E1, E2, E3, P0, P1, P2, P3, N0, N1, N2, N3, CLS;
   static constexpr M VALID = (M)(0x8888888888888888ULL >> (64 - 4 * NC));
 
-  __device__ __forceinline__ static uint32_t partner(uint32_t e) { return e ? (((e - 1u) ^ 1u) + 1u) : 15u; }
 
   // face labels and partners of every candidate (E, P); build() adds the rest.
   // Candidate (t, r) shows lab[4t + ((k - r) & 3)] on side k, so tile t's 16-bit chunk of
@@ -213,7 +212,7 @@ template <typename M, int NC, bool STRICT> struct CandSwar {
       for (int k = 0; k < 4; k++) S[k] |= in << get_nib<M>(E[(k + 2) & 3], c);
     }
     // per candidate, nibble-flag form (bit 4k+3 <-> side k): sides that can bond it, zero faces;
-    // packed partner labels (partner() is injective, so equal packs <=> equal codes, _k:199)
+    // packed partner labels (the partner map is injective, so equal packs <=> equal codes, _k:199)
     uint32_t bond[NC], z[NC], pc[NC];
 #pragma unroll
     for (int c = 0; c < NC; c++) {
