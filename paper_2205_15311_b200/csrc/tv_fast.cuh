@@ -1,14 +1,17 @@
 // tv_fast.cuh -- the enumeration hot kernel: lane-per-genome movelist assembly
 // on a shared-memory nibble board with per-genome candidate tables.
 //
-// Covers a <= 3 tile types, b <= 8 labels, d with (d+2)^2 < 2^16.
+// Covers a <= 3 tile types, b <= 8 labels, d <= 118 (row stride < 128).
 // Bit-exact with the reference step order (_k:96-249).
 //
-// Layout (per warp, word-interleaved so lane L always hits bank L):
+// Layout (per warp, interleaved by lane so lane L always hits bank L):
 //   board : GW words/lane; cell (r,c) of the (d+2)x(d+2) padded board is
-//           nibble lin = r*(d+2)+c; 0..4a-1 = placed candidate t*4+orient,
-//           0xE = empty + on the movelist, 0xF = empty.
-//   stack : S u16 entries/lane (entry = lin), spilled to global beyond S.
+//           nibble lin = r*RS+c (RS = 8*ceil((d+2)/8) for a <= 2: whole-word
+//           rows, N/S neighbours at a fixed word offset; RS = d+2 for a = 3);
+//           0..4a-1 = placed candidate t*4+orient, 0xE = empty + on the
+//           movelist, 0xF = empty.
+//   stack : S u16 entries/lane (entry = lin; entry j of lane L at halfword
+//           j*32+L), spilled to global beyond S.
 // Per CTA: a small open-addressed phenotype cache (histogram mode) and the
 // class tallies, flushed to the global table once at the end.
 //
