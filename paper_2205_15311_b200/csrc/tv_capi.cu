@@ -198,8 +198,8 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
     size_t smem = fast_smem_bytes(threads, P.GW, P.S, P.cta_slots, P.q);
     int maxsmem = 0;
     CK(cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    while (smem > (size_t)maxsmem && threads > 32) {
-      threads /= 2;
+    while (smem > (size_t)maxsmem && threads > 32) {  // whole warps only (the kernel's ballots)
+      threads -= 32;
       smem = fast_smem_bytes(threads, P.GW, P.S, P.cta_slots, P.q);
     }
     if (smem <= (size_t)maxsmem) {

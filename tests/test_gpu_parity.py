@@ -245,3 +245,25 @@ def test_enumerate_full_s28_other_seeds_vs_oracle(K, seed, strict):
     for k in ("keys", "det", "steric", "rep_det", "rep_any", "w", "h", "cells", "tallies"):
         assert np.array_equal(getattr(h, k).astype(np.int64), getattr(acc, k).astype(np.int64)), k
     assert np.array_equal(h.shape, acc.shape)
+
+
+@pytest.mark.parametrize("d,path", [(61, "bitboard"), (105, "bitboard"), (117, None), (119, "generic")])
+def test_large_grid_path_boundary_vs_oracle(K, d, path):
+    """Large grids: the bitboard kernel runs while whole warps' boards fit in shared memory
+    (fewer lanes per CTA as d grows; d <= 118 for byte cell offsets), beyond that the generic
+    kernel; every case equals the oracle row for row (long runs, deep movelists that spill)."""
+    from oracle import oracle as O
+    from paper_2205_15311_b200 import _lib
+    rng = np.random.default_rng(d)
+    idx = np.sort(rng.choice(1 << 24, 384, replace=False)).astype(np.uint64)
+    args = (2, 3, np.zeros(0, np.int64), np.zeros(0, np.uint8), np.arange(23, -1, -1, dtype=np.int64))
+    ks = np.array([1, 2])
+    W = ((d - 2) ** 2 + 63) // 64  # shape rows wide enough for the largest crop
+    g = G.fresh_outputs(idx.shape[0], 2, W)
+    o = G.fresh_outputs(idx.shape[0], 2, W)
+    K.classify_batch(idx, *args, d, ks, 2, np.uint64(3), True, *[g[k] for k in G.OUT_KEYS])
+    if path is not None:
+        assert _lib.launch_info()["path"] == path
+    O.classify_batch(idx, *args, d, ks, 2, 3, True, *[o[k] for k in G.OUT_KEYS])
+    for k in G.OUT_KEYS:
+        assert np.array_equal(g[k], o[k]), k
