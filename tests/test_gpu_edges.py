@@ -192,3 +192,39 @@ def test_device_exchange_rows_equal_single_histogram(M, space, ks, chunk):
     parts[1].replace_rows(torch.cat(rows), tal)
     got = parts[1].export()
     assert got == exp
+
+
+@pytest.mark.parametrize("d", [41, 97])
+def test_histogram_mode_large_grid_vs_oracle(M, d):
+    """Histogram mode on large grids (fewer lanes per CTA, wide shape rows) equals the
+    aggregation of the oracle's per-genome rows."""
+    from oracle import oracle as O
+    K, L, C, Gm = M
+    idx = np.arange(0x71000, 0x71000 + (1 << 13), dtype=np.uint64)
+    W = ((d - 2) ** 2 + 63) // 64
+    ks = (1, 2, 4)
+    o = G.fresh_outputs(idx.shape[0], len(ks), W)
+    O.classify_batch(idx, *S28_ARGS, d, np.array(ks), 4, 0, True, *[o[k] for k in G.OUT_KEYS])
+    exp = C.Histogram.from_rows(idx, *[o[k] for k in G.OUT_KEYS], ks=ks, hist_k=4, W=W)
+    dh = C.DeviceHistogram(ks, 4, W, 1 << 14)
+    dh.enumerate_range(Gm.SearchSpace(2, 8), int(idx[0]), idx.shape[0], d, 0, True)
+    got = dh.export()
+    for k in ("keys", "det", "steric", "rep_det", "rep_any", "w", "h", "cells", "tallies"):
+        assert np.array_equal(getattr(got, k).astype(np.int64), getattr(exp, k).astype(np.int64)), k
+    assert np.array_equal(got.shape, exp.shape)
+
+
+def test_generic_kernel_large_grid_vs_oracle(M):
+    """d = 151 (generic kernel: beyond the bitboard's shared-memory board) equals the oracle."""
+    from oracle import oracle as O
+    K, L, C, Gm = M
+    d = 151
+    idx = np.arange(0x3A0000, 0x3A0000 + 96, dtype=np.uint64)
+    W = ((d - 2) ** 2 + 63) // 64
+    g = G.fresh_outputs(idx.shape[0], 2, W)
+    o = G.fresh_outputs(idx.shape[0], 2, W)
+    K.classify_batch(idx, *S28_ARGS, d, np.array([1, 3]), 3, np.uint64(5), False, *[g[k] for k in G.OUT_KEYS])
+    assert L.launch_info()["path"] == "generic"
+    O.classify_batch(idx, *S28_ARGS, d, np.array([1, 3]), 3, 5, False, *[o[k] for k in G.OUT_KEYS])
+    for k in G.OUT_KEYS:
+        assert np.array_equal(g[k], o[k]), k
