@@ -228,3 +228,39 @@ def test_generic_kernel_large_grid_vs_oracle(M):
     O.classify_batch(idx, *S28_ARGS, d, np.array([1, 3]), 3, 5, False, *[o[k] for k in G.OUT_KEYS])
     for k in G.OUT_KEYS:
         assert np.array_equal(g[k], o[k]), k
+
+
+@pytest.mark.parametrize("strict", [False, True])
+def test_s32_random_nonstrict_and_strict_vs_oracle(M, strict):
+    """a = 3 (64-bit candidate planes) under both contact rules, 4096 random S32 genomes, k up to 8."""
+    from oracle import oracle as O
+    K, L, C, Gm = M
+    sp = Gm.space_from_preset("s32_3_8")
+    a, bpl, mp, mv, fp = sp.kernel_args()
+    idx = np.sort(np.random.default_rng(32 + strict).choice(1 << 32, 4096, replace=False)).astype(np.uint64)
+    ks = np.array([1, 4, 8])
+    g = G.fresh_outputs(idx.shape[0], 3)
+    o = G.fresh_outputs(idx.shape[0], 3)
+    K.classify_batch(idx, a, bpl, mp, mv, fp, 19, ks, 8, np.uint64(99), strict, *[g[k] for k in G.OUT_KEYS])
+    O.classify_batch(idx, a, bpl, mp, mv, fp, 19, ks, 8, 99, strict, *[o[k] for k in G.OUT_KEYS])
+    for k in G.OUT_KEYS:
+        assert np.array_equal(g[k], o[k]), k
+
+
+def test_histogram_mode_a1_full_space_vs_oracle(M):
+    """a = 1: the whole S_{1,8} (4096 genomes) into the device histogram with k = 16 prefixes."""
+    from oracle import oracle as O
+    K, L, C, Gm = M
+    sp = Gm.SearchSpace(1, 8)
+    a, bpl, mp, mv, fp = sp.kernel_args()
+    idx = np.arange(sp.cardinality, dtype=np.uint64)
+    ks = (1, 2, 4, 8, 16)
+    o = G.fresh_outputs(idx.shape[0], len(ks), 5)
+    O.classify_batch(idx, a, bpl, mp, mv, fp, 19, np.array(ks), 16, 0, True, *[o[k] for k in G.OUT_KEYS])
+    exp = C.Histogram.from_rows(idx, *[o[k] for k in G.OUT_KEYS], ks=ks, hist_k=16, W=5)
+    dh = C.DeviceHistogram(ks, 16, 5, 1 << 12)
+    dh.enumerate_range(sp, 0, sp.cardinality, 19, 0, True)
+    got = dh.export()
+    for k in ("keys", "det", "steric", "rep_det", "rep_any", "w", "h", "cells", "tallies"):
+        assert np.array_equal(getattr(got, k).astype(np.int64), getattr(exp, k).astype(np.int64)), k
+    assert np.array_equal(got.shape, exp.shape)
