@@ -256,3 +256,37 @@ def test_replicas_final_population_and_init():
         k, *_ = O.ga_run(pop, L, 2, T, int(seeds[r]), 5, gens, 30, n // 2, 0)
         assert k == done[r] == gens
         assert np.array_equal(fin[r], pop), r
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", [0, 1])
+def test_jatam_generations_external_fitness_vs_restatement(mode):
+    """The JaTAM GA loop: device fitness (checked against the oracle above) feeds one external-
+    fitness generation at a time; each child equals the CPU restatement's child drawn from the
+    same integer CDF (oracle ga_child), stats included, for several generations."""
+    from paper_2205_15311_b200._kernels import edges_from_labels
+    from paper_2205_15311_b200.genome import SearchSpace, decode_tileset, genome_at_index
+    S28 = SearchSpace(2, 8)
+    d, k, n, L, lam = 19, 8, 1000, 24, 0.5
+    tgt_idx = 0x801772
+    ts = decode_tileset(genome_at_index(S28, tgt_idx), S28)
+    e = edges_from_labels(np.array([v for t in ts.tiles for v in t], np.uint8), 2)
+    grid = np.empty(d * d, np.int16)
+    O.assemble_single(e, 2, d, 0, tgt_idx, 0, True, grid)
+    target = (grid >= 0).reshape(d, d)
+    pop = np.random.default_rng(5).integers(0, 1 << 24, n, dtype=np.uint64)
+    pop[:10] = tgt_idx  # some fit individuals
+    ga = E.DeviceGA(n, L, lam, mode)
+    ga.set_population(pop)
+    T = E.poisson_thresholds(lam, L)
+    for g in range(4):
+        f = ga.jatam_fitness(S28, target, d, k)
+        fh = f.cpu().numpy().view(np.uint32).astype(np.uint64)
+        cdf = np.cumsum(fh).astype(np.uint64)
+        kk, b, s, c = ga.run(21, g, 1, 300, n, 0, f_ext=f)
+        assert kk == 1 and int(b[0]) == int(fh.max()) and int(s[0]) == int(fh.sum())
+        assert int(c[0]) == int(np.count_nonzero(fh >= 300))
+        exp = np.array([O.ga_child(21, g, i, pop, cdf, L, mode, T) for i in range(n)], np.uint64)
+        pop = ga.population()
+        assert np.array_equal(pop, exp), g
+    ga.close()
