@@ -264,3 +264,23 @@ def test_histogram_mode_a1_full_space_vs_oracle(M):
     for k in ("keys", "det", "steric", "rep_det", "rep_any", "w", "h", "cells", "tallies"):
         assert np.array_equal(getattr(got, k).astype(np.int64), getattr(exp, k).astype(np.int64)), k
     assert np.array_equal(got.shape, exp.shape)
+
+
+@pytest.mark.parametrize("d", [61, 181])
+def test_single_genome_apis_large_grid_vs_oracle(M, d):
+    """classify_single / assemble_single (one device thread) on large grids: line-prone tile
+    sets grow long runs; every return value, the shape words and the grid equal the oracle."""
+    from oracle import oracle as O
+    K, L, C, Gm = M
+    rng = np.random.default_rng(d)
+    W = ((d - 2) ** 2 + 63) // 64
+    for t in range(12):
+        labels = rng.integers(0, 8, 8).astype(np.uint8)
+        labels[2] = ((labels[0] - 1) ^ 1) + 1 if labels[0] else 1  # tile 0 bonds itself N-S: long runs
+        e = K.edges_from_labels(labels, 2)
+        sw_g, sw_o = np.zeros(W, np.uint64), np.zeros(W, np.uint64)
+        assert K.classify_single(e, 2, d, 4, 7, t, True, sw_g) == O.classify_single(e, 2, d, 4, 7, t, True, sw_o)
+        assert np.array_equal(sw_g, sw_o)
+        gg, go = np.empty(d * d, np.int16), np.empty(d * d, np.int16)
+        assert K.assemble_single(e, 2, d, 7, t, 1, False, gg) == O.assemble_single(e, 2, d, 7, t, 1, False, go)
+        assert np.array_equal(gg, go)
