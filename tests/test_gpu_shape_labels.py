@@ -82,3 +82,30 @@ def test_empty_and_oversized_rows(C):
     rot4, d4 = C.shape_labels(np.array([9, 2], np.uint8), np.array([9, 2], np.uint8),
                               np.array([[~np.uint64(0)], [np.uint64(15)]], np.uint64))
     assert rot4[0] == 0 and d4[0] == 0 and rot4[1] != 0
+
+
+def test_labels_large_shapes(C):
+    """Crops of large grids (up to 120 x 120, W = 225 words) against the host definitions,
+    D4 invariance included."""
+    rng = np.random.default_rng(29)
+    shapes = []
+    for _ in range(40):
+        w, h = int(rng.integers(1, 121)), int(rng.integers(1, 121))
+        b = rng.random((h, w)) < rng.uniform(0.05, 0.6)
+        b[0, rng.integers(0, w)] = True
+        b[rng.integers(0, h), 0] = True
+        shapes.append(C.CroppedShape(w, h, b))
+    W = (120 * 120 + 63) // 64
+    for variant in (0, 1, 5):
+        vs = [s.rotated(variant & 3) if variant < 4 else s.mirrored().rotated(variant & 3) for s in shapes]
+        w = np.array([s.width for s in vs], np.uint8)
+        h = np.array([s.height for s in vs], np.uint8)
+        sh = np.stack([s.packed_words(W) for s in vs])
+        rot4, d4 = C.shape_labels(w, h, sh)
+        if variant == 0:
+            hr, hd = _host_labels(C, w, h, sh)
+            assert np.array_equal(rot4, hr) and np.array_equal(d4, hd)
+            base_r, base_d = rot4, d4
+        assert np.array_equal(d4, base_d)
+        if variant < 4:
+            assert np.array_equal(rot4, base_r)
