@@ -52,7 +52,7 @@ def test_histogram_refuses_other_parameters(M):
     assert dh.export().total == 4096
 
 
-@pytest.mark.parametrize("ks,hist_k", [((1, 2, 4, 8), 4), ((2, 8), 2), ((8,), 8)])
+@pytest.mark.parametrize("ks,hist_k", [((1, 2, 4, 8), 4), ((2, 8), 2), ((8,), 8), ((1,), 1), ((3,), 3), ((2, 5), 5)])
 def test_histogram_mode_hist_k_below_kmax(M, ks, hist_k):
     """Histogram = aggregation of the oracle's per-genome rows for prefix ks with hist_k < ks[-1]."""
     from oracle import oracle as O
