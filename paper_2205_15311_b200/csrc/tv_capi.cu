@@ -337,6 +337,7 @@ __global__ void __launch_bounds__(256) k_int_peak(int64_t iters, uint32_t seed, 
 }  // namespace
 
 struct tv_hist {
+  void *block = nullptr;  // the single device allocation holding every table of H
   HistDev H;
   int device;
   bool has_params = false;  // enumeration parameters of the genomes counted since the last clear
@@ -597,18 +598,22 @@ int tv_hist_create(int64_t capacity, int32_t q, int32_t W, tv_hist **out) {
   h->device = dev;
   HistDev &H = h->H;
   H.cap = cap; H.W = W; H.q = q;
-  cudaError_t e = cudaSuccess;
-  e = e ? e : cudaMalloc(&H.keys, cap * 8);
-  e = e ? e : cudaMalloc(&H.det, cap * 8);
-  e = e ? e : cudaMalloc(&H.steric, cap * 8);
-  e = e ? e : cudaMalloc(&H.rep_det, cap * 8);
-  e = e ? e : cudaMalloc(&H.rep_any, cap * 8);
-  e = e ? e : cudaMalloc(&H.whc, cap * 4);
-  e = e ? e : cudaMalloc(&H.pay_idx, cap * 8);
-  e = e ? e : cudaMalloc(&H.shape, cap * 8 * W);
-  e = e ? e : cudaMalloc(&H.tallies, (size_t)q * 5 * 8);
-  e = e ? e : cudaMalloc(&H.n_keys, 4);
-  e = e ? e : cudaMalloc(&H.overflow, 4);
+  // one allocation carved into the tables (one cudaMalloc / cudaFree per histogram)
+  const size_t sizes[11] = {(size_t)cap * 8, (size_t)cap * 8, (size_t)cap * 8, (size_t)cap * 8, (size_t)cap * 8,
+                            (size_t)cap * 4, (size_t)cap * 8, (size_t)cap * 8 * W, (size_t)q * 5 * 8, 4, 4};
+  size_t total = 0;
+  for (size_t sz : sizes) total += (sz + 255) & ~(size_t)255;
+  cudaError_t e = cudaMalloc(&h->block, total);
+  if (e == cudaSuccess) {
+    char *p = static_cast<char *>(h->block);
+    void **dst[11] = {(void **)&H.keys, (void **)&H.det, (void **)&H.steric, (void **)&H.rep_det,
+                      (void **)&H.rep_any, (void **)&H.whc, (void **)&H.pay_idx, (void **)&H.shape,
+                      (void **)&H.tallies, (void **)&H.n_keys, (void **)&H.overflow};
+    for (int i = 0; i < 11; i++) {
+      *dst[i] = p;
+      p += (sizes[i] + 255) & ~(size_t)255;
+    }
+  }
   if (e != cudaSuccess) {
     tv_hist_destroy(h);
     return fail(TV_ERR_CUDA, "histogram allocation: %s", cudaGetErrorString(e));
@@ -622,9 +627,8 @@ int tv_hist_create(int64_t capacity, int32_t q, int32_t W, tv_hist **out) {
 int tv_hist_destroy(tv_hist *h) {
   if (!h) return 0;
   HistDev &H = h->H;
-  cudaFree(H.keys); cudaFree(H.det); cudaFree(H.steric); cudaFree(H.rep_det); cudaFree(H.rep_any);
-  cudaFree(H.whc); cudaFree(H.pay_idx); cudaFree(H.shape); cudaFree(H.tallies); cudaFree(H.n_keys);
-  cudaFree(H.overflow);
+  (void)H;
+  if (h->block) cudaFree(h->block);
   delete h;
   return 0;
 }
