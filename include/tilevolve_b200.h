@@ -64,7 +64,7 @@ const char *tv_last_error(void);
 
 /* Kernel-path statistics of the last enumerate / classify launch on this
  * thread: [0] path (1 = shared-memory bitboard kernel: a <= 3, bits per label <= 3,
- * d <= 118; 2 = generic kernel: everything else), 
+ * d <= 118; 2 = generic kernel: everything else),
  * [1] CTAs, [2] threads per CTA, [3] dynamic shared bytes per CTA,
  * [4] launches issued by the call. */
 int tv_last_launch_info(int64_t *info5);
