@@ -559,6 +559,7 @@ def main():
         print(json.dumps(line), flush=True)
     hist.close()
     if world > 1:
+        dist.barrier()  # the other ranks wait for rank 0's single-GPU legs before tearing down
         dist.destroy_process_group()
 
 
