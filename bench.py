@@ -554,7 +554,9 @@ def main():
                 "e2e": {"value": N_S28 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                         "d2h_bytes_per_step": int(d2h), "api": "classify.enumerate_space"},
                 "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(),
-                "gpu_launches": 3 * args.steps, "s32": s32, "ga": ga, "ga_jatam": ga_jatam,
+                # ours per step: k_hist_reset, k_prepass, k_classify_fast (+ at N > 1 the exchange:
+                # k_hist_compact, k_hist_pack, k_hist_reset, k_hist_merge, k_hist_merge_rows1/2)
+                "gpu_launches": (3 if world == 1 else 9) * args.steps, "s32": s32, "ga": ga, "ga_jatam": ga_jatam,
                 "ga_sweep": ga_sweep}
         print(json.dumps(line), flush=True)
     hist.close()
