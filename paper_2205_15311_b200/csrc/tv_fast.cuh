@@ -43,7 +43,10 @@ template <typename M> __device__ __forceinline__ uint32_t get_nib(M x, uint32_t 
   return (uint32_t)(x >> (4 * i)) & 15u;
 }
 __device__ __forceinline__ int ffs_m(uint32_t x) { return __ffs(x) - 1; }
-__device__ __forceinline__ int ffs_m(uint64_t x) { return __ffsll((long long)x) - 1; }
+__device__ __forceinline__ int ffs_m(uint64_t x) {  // candidate flags never reach bit 63: halves suffice
+  const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+  return lo ? __ffs(lo) - 1 : 31 + __ffs(hi);
+}
 
 struct FastLane {
   uint32_t *gw;     // &board word 0 of this lane (stride 32 words)
