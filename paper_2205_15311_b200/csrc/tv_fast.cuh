@@ -35,9 +35,17 @@ namespace tvb {
 template <typename M> __device__ __forceinline__ M rep_nib(uint32_t v) {
   return (M)v * (M)0x1111111111111111ULL;
 }
+template <> __device__ __forceinline__ uint64_t rep_nib<uint64_t>(uint32_t v) {  // v < 16: one multiply
+  const uint32_t r = v * 0x11111111u;
+  return ((uint64_t)r << 32) | r;
+}
 template <typename M> __device__ __forceinline__ M nz_nib(M x) {  // bit 4i+3 set iff nibble i != 0
   const M l7 = (M)0x7777777777777777ULL, l8 = (M)0x8888888888888888ULL;
   return (((x & l7) + l7) | x) & l8;
+}
+template <> __device__ __forceinline__ uint64_t nz_nib<uint64_t>(uint64_t x) {  // no carry crosses a nibble
+  const uint32_t lo = nz_nib<uint32_t>((uint32_t)x), hi = nz_nib<uint32_t>((uint32_t)(x >> 32));
+  return ((uint64_t)hi << 32) | lo;
 }
 template <typename M> __device__ __forceinline__ uint32_t get_nib(M x, uint32_t i) {
   return (uint32_t)(x >> (4 * i)) & 15u;
