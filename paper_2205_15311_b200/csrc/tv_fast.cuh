@@ -165,12 +165,11 @@ template <typename M, int NC, bool STRICT> struct CandSwar {
     const uint32_t pE = (uint32_t)(((uint64_t)E3 >> sE) & 15u);
     const uint32_t pS = (uint32_t)(((uint64_t)E0 >> sS) & 15u);
     const uint32_t pW = (uint32_t)(((uint64_t)E1 >> sW) & 15u);
-    const M l7 = (M)0x7777777777777777ULL;
     M bond = 0, conf = 0;
 #define TV_DIR(Pd, Nd, p)                                                    \
   {                                                                          \
     const M x = (Pd) ^ rep_nib<M>(p);                                        \
-    const M bm = ~((((x & l7) + l7) | x)) & VALID;                           \
+    const M bm = ~nz_nib<M>(x) & VALID; /* nibble == 0 */                    \
     bond |= bm;                                                              \
     if (STRICT) conf |= (p) ? ((Nd) & ~bm) : (M)0;                           \
   }
