@@ -8,6 +8,8 @@ timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
   > /dev/null 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_classify_fast|k_prepass|k_shape_labels" \
   -c 4 -o gpurun_out/enum_full python tools/enum_once.py s28 > gpurun_out/ncu_enum.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_classify_fast|k_prepass" -c 2 \
+  -o gpurun_out/enum32_full python tools/enum_once.py s32 > gpurun_out/ncu_enum32.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k k_ga_run -c 1 \
   -o gpurun_out/ga_full python tools/prof_ga.py --gens 200 > gpurun_out/ncu_ga.log 2>&1
 tail -n 2 gpurun_out/ncu_enum.log; tail -n 2 gpurun_out/ncu_ga.log

@@ -57,4 +57,11 @@ ga_lines = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_line
                            os.path.join(OUT, "ga_full.ncu-rep"), "40"], capture_output=True, text=True).stdout
 with open(os.path.join(PROF, f"{tag}_lines_ga.txt"), "w") as f:
     f.write(ga_lines)
+rep32 = os.path.join(OUT, "enum32_full.ncu-rep")  # a = 3 kernel (S32 block), when captured
+if os.path.exists(rep32):
+    details(rep32, os.path.join(PROF, f"{tag}_ncu_full_enum32_details.csv"))
+    l32 = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_lines.py"), rep32, "60", "k_classify_fast"],
+                         capture_output=True, text=True).stdout
+    with open(os.path.join(PROF, f"{tag}_lines_enum32.txt"), "w") as f:
+        f.write(l32)
 print(json.dumps(traffic, indent=1))
