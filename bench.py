@@ -7,9 +7,10 @@ all in the sm_100a bitboard kernel.  With N ranks the index range is dealt out
 in round-robin chunks (strong scaling: the job is always the whole space) and
 the per-rank histograms are combined with one device-resident NCCL exchange
 (paper_2205_15311_b200.distributed.allreduce_device_histogram: raw rows packed on
-the GPU, one all_gather + one all_reduce over NVLink, merge on the GPU) inside the
-step; at every N the step ends with the whole-space histogram resident on the GPU
-(the host export is part of e2e).
+the GPU and cut by owning rank = hash mod N, one all_to_all + one all_reduce over
+NVLink, owner-side merge on the GPU) inside the step; at every N the step ends with
+the whole-space histogram resident on the GPU(s), sharded by key for N > 1 (the host
+export and gather are part of e2e).
 
   value : device-timed (CUDA events, max over ranks) genomes/s, no host I/O.
   e2e   : the same job through the public API classify.enumerate_space (host
@@ -250,7 +251,7 @@ def s32_bench(args, rank: int, world: int, stream) -> dict:
     import torch.distributed as dist
     from paper_2205_15311_b200 import _lib
     from paper_2205_15311_b200.classify import DeviceHistogram, shape_words_for
-    from paper_2205_15311_b200.distributed import allreduce_device_histogram
+    from paper_2205_15311_b200.distributed import allreduce_device_histogram, gather_sharded
     from paper_2205_15311_b200.genome import space_from_preset
 
     L = _lib.lib()
@@ -275,7 +276,7 @@ def s32_bench(args, rank: int, world: int, stream) -> dict:
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     run(mine * chunk)
-    if world > 1:  # the merged histogram stays on every GPU, as the 1-GPU one does
+    if world > 1:  # the merged histogram stays on the GPUs, sharded by key
         allreduce_device_histogram(hist, None, export=False)
     e1.record(stream)
     torch.cuda.synchronize()
@@ -283,6 +284,8 @@ def s32_bench(args, rank: int, world: int, stream) -> dict:
     if world > 1:
         ms = max_over_ranks(ms)
     final = hist.export(sp)
+    if world > 1:  # each GPU holds its key shard of the merged histogram: gather for the check
+        final = gather_sharded(final, None)
     hist.close()
     try:
         gold = json.load(open(os.path.join(ROOT, "tests", "golden", "hist_s32_full.json")))
@@ -412,7 +415,8 @@ def main():
             dist.init_process_group(backend, rank=rank, world_size=world)
     from paper_2205_15311_b200 import _lib
     from paper_2205_15311_b200.classify import DeviceHistogram, enumerate_space, shape_words_for
-    from paper_2205_15311_b200.distributed import allreduce_device_histogram, enumerate_space_distributed
+    from paper_2205_15311_b200.distributed import (allreduce_device_histogram, enumerate_space_distributed,
+                                                   gather_sharded)
 
     L = _lib.lib()
     space = s28_space()
@@ -460,7 +464,7 @@ def main():
             _lib.check(L.tv_enumerate_chunks(rank * CHUNK, count, CHUNK, CHUNK * world, a, bpl, _lib.ptr(mp),
                                              _lib.ptr(mv), mp.shape[0], _lib.ptr(fp), fp.shape[0], 19, _lib.ptr(ks),
                                              ks.shape[0], 8, 0, 1, hist._h, sp))
-            if world > 1:  # timed region ends, at every N, with the merged histogram on the GPU
+            if world > 1:  # timed region ends, at every N, with the merged histogram on the GPU(s)
                 allreduce_device_histogram(hist, None, export=False)
             e2.record(stream)
         barrier()
@@ -475,6 +479,8 @@ def main():
 
     # correctness of what was timed: the exported histogram equals the reference aggregate
     final = hist.export(sp)
+    if world > 1:
+        final = gather_sharded(final, None)
     tallies_ok = final.tallies.tolist() == [[7448198, 5894957, 0, 3434061, 0], [6939346, 6865723, 214055, 2758092, 0],
                                             [6697803, 7791627, 223880, 2063906, 0], [6631160, 8336639, 199388, 1610029, 0]]
 

@@ -17,6 +17,7 @@ the order DET, TRIV, STERIC, UNB, ERROR.
 from __future__ import annotations
 
 import ctypes
+import hashlib
 import io
 import json
 import math
@@ -241,7 +242,7 @@ class Histogram:
         np.minimum.at(out.rep_det, inv[isdet], idx[sel][isdet])
         # payload = the representative's row (lowest index per key), whatever the row order
         order = np.lexsort((idx[sel], inv))
-        starts = np.r_[0, np.flatnonzero(np.diff(inv[order])) + 1]
+        starts = np.r_[0, np.flatnonzero(np.diff(inv[order])) + 1] if sel.size else np.zeros(0, np.int64)
         rows = sel[order[starts]]
         out.w = np.asarray(out_w)[rows].astype(np.uint8)
         out.h = np.asarray(out_h)[rows].astype(np.uint8)
@@ -571,20 +572,35 @@ def enumerate_space(space: SearchSpace, d: int = 19, k: int = 8, seed: int = 0, 
     hist_k = int(hist_k if hist_k is not None else ks[-1])
     if count is None:
         count = space.cardinality - start
+    if start < 0 or count < 0 or start + count > space.cardinality:
+        raise ValueError(f"[start, start+count) = [{start}, {start + count}) is outside the space "
+                         f"(cardinality {space.cardinality})")
     W = shape_words_for(d)
     plan = chunks if chunks is not None else chunk_plan(start, count, batch_size)
+    for s_, n_ in plan:
+        if s_ < 0 or n_ < 0 or s_ + n_ > space.cardinality:
+            raise ValueError(f"chunk ({s_}, {n_}) is outside the space (cardinality {space.cardinality})")
     meta = _space_meta(space, d, seed, strict)
+    # the chunk cursor of a checkpoint only means something for the very same plan
+    cursor = dict(start=int(start), count=int(count), batch_size=int(batch_size), chunks_total=len(plan),
+                  plan_sha256=hashlib.sha256(json.dumps([[int(a), int(b)] for a, b in plan]).encode()).hexdigest())
     dev = _cached_histogram(ks, hist_k, W, capacity)
     done = 0
     if resume:
         prev, extra = Histogram.load(resume)
         if prev.ks != ks or prev.hist_k != hist_k or prev.W != W:
             raise ValueError("checkpoint was written with different ks / hist_k / d")
-        for key in ("a", "b", "d", "seed", "strict"):
+        for key in ("a", "b", "fixed_mask", "d", "seed", "strict"):
             if prev.meta.get(key) != meta[key]:
                 raise ValueError(f"checkpoint parameter {key} differs")
-        dev.merge(prev)
+        for key, v in cursor.items():
+            if extra.get(key) != v:
+                raise ValueError(f"checkpoint was written for another chunk plan ({key}: {extra.get(key)!r} "
+                                 f"!= {v!r})")
         done = int(extra["chunks_done"])
+        if not 0 <= done <= len(plan):
+            raise ValueError(f"checkpoint cursor {done} outside the plan of {len(plan)} chunks")
+        dev.merge(prev)
     t0 = time.time()
     try:
         for ci in range(done, len(plan)):
@@ -593,7 +609,7 @@ def enumerate_space(space: SearchSpace, d: int = 19, k: int = 8, seed: int = 0, 
             if progress is not None:
                 progress(ci + 1, len(plan))
             if checkpoint and ((ci + 1) % checkpoint_every == 0 or ci + 1 == len(plan)):
-                dev.export(meta=meta).save(checkpoint, extra=dict(chunks_done=ci + 1, chunks_total=len(plan)))
+                dev.export(meta=meta).save(checkpoint, extra=dict(cursor, chunks_done=ci + 1))
         out = dev.export(meta=meta)
     except BaseException:
         _drop_cached_histogram(dev)

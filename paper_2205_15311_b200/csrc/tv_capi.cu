@@ -858,11 +858,25 @@ static int enumerate_common(const uint64_t *indices, uint64_t start, uint64_t ch
   return 0;
 }
 
+// The space has 2^nfree indices; the decoder ignores index bits >= nfree, so an index
+// past the end would alias (idx mod 2^nfree) and be counted twice: reject it.
+static int check_last_index(uint64_t last, int64_t nfree) {
+  if (nfree < 0 || nfree > 64) return fail(TV_ERR_ARG, "nfree=%lld outside [0, 64]", (long long)nfree);
+  if (nfree < 64 && last >= ((uint64_t)1 << nfree))
+    return fail(TV_ERR_ARG, "index %llu is outside the space (2^%lld indices)", (unsigned long long)last,
+                (long long)nfree);
+  return 0;
+}
+
 int tv_enumerate_range(uint64_t start, uint64_t count, int32_t a, int32_t bpl, const int64_t *mask_pos,
                        const uint8_t *mask_val, int64_t m, const int64_t *free_pos, int64_t nfree, int32_t d,
                        const int64_t *ks, int64_t q, int32_t hist_k, uint64_t seed, int32_t strict, tv_hist *h,
                        void *stream) {
   if (count > ((uint64_t)1 << 62)) return fail(TV_ERR_ARG, "count too large for one call");
+  if (count > 0) {
+    if (start + (count - 1) < start) return fail(TV_ERR_ARG, "index range wraps around 2^64");
+    if (int rc = check_last_index(start + (count - 1), nfree)) return rc;
+  }
   return enumerate_common(nullptr, start, 0, 0, (int64_t)count, a, bpl, mask_pos, mask_val, m, free_pos, nfree, d, ks, q,
                           hist_k, seed, strict, h, stream);
 }
@@ -873,6 +887,13 @@ int tv_enumerate_chunks(uint64_t start, uint64_t count, uint64_t chunk, uint64_t
                         int32_t strict, tv_hist *h, void *stream) {
   if (count > ((uint64_t)1 << 62)) return fail(TV_ERR_ARG, "count too large for one call");
   if (chunk == 0 || stride < chunk) return fail(TV_ERR_ARG, "need 0 < chunk <= stride");
+  if (count > 0) {
+    const uint64_t c = (count - 1) / chunk, r = (count - 1) % chunk;  // the last item's chunk and offset
+    if (c > 0 && stride > (~0ULL - start) / c) return fail(TV_ERR_ARG, "chunk layout wraps around 2^64");
+    const uint64_t last = start + c * stride;
+    if (last + r < last) return fail(TV_ERR_ARG, "chunk layout wraps around 2^64");
+    if (int rc = check_last_index(last + r, nfree)) return rc;
+  }
   return enumerate_common(nullptr, start, chunk, stride, (int64_t)count, a, bpl, mask_pos, mask_val, m, free_pos,
                           nfree, d, ks, q, hist_k, seed, strict, h, stream);
 }

@@ -390,9 +390,34 @@ def run_replicas(cfg: GAConfig, seeds) -> list[RunRecord]:
     return out
 
 
+def censored_median_ci(vals, cutoff: int, sample_size: int = 100, resamples: int = 10000, rng=None) -> dict:
+    """Median + bootstrap CI of per-run times with cutoff censoring.
+
+    ``vals`` holds one entry per run, None = censored at the cutoff.  When at most
+    half the runs are censored they stay in the sample as ">= cutoff" (value
+    ``cutoff``, which keeps their rank: every uncensored time is < cutoff), in the
+    median and in every bootstrap resample; a median or CI bound that lands on a
+    censored value is itself only a lower bound, flagged ``*_censored``.  When more
+    than half are censored the median is reported as censored (None)."""
+    n = len(vals)
+    cens = sum(v is None for v in vals)
+    if n == 0:
+        raise ValueError("vals must be non-empty")
+    if cens * 2 > n:
+        return dict(median=None, ci_lo=None, ci_hi=None, censored=cens, median_censored=True,
+                    ci_lo_censored=True, ci_hi_censored=True)
+    x = [float(cutoff) if v is None else float(v) for v in vals]
+    med, lo, hi = bootstrap_median_ci(x, sample_size, resamples, rng)
+    return dict(median=med, ci_lo=lo, ci_hi=hi, censored=cens, median_censored=bool(cens and med >= cutoff),
+                ci_lo_censored=bool(cens and lo >= cutoff), ci_hi_censored=bool(cens and hi >= cutoff))
+
+
 def sweep(mu_L_grid, runs: int = 100, base: GAConfig | None = None, seed0: int = 0, sample_size: int = 100,
-          resamples: int = 10000) -> list[dict]:
-    """SPEC:452 sweep JSON rows: {muL, runs, discovery:{median, ci_lo, ci_hi, censored}, adaptation:{...}}."""
+          resamples: int = 10000, out: str | None = None) -> list[dict]:
+    """SPEC:452 sweep rows: {muL, runs, discovery:{median, ci_lo, ci_hi, censored}, adaptation:{...}}.
+
+    Censoring follows SPEC:448 (``censored_median_ci``).  With ``out`` the rows are
+    written as the sweep JSON artefact, together with the configuration."""
     base = base or GAConfig()
     rows = []
     for mu in mu_L_grid:
@@ -402,12 +427,35 @@ def sweep(mu_L_grid, runs: int = 100, base: GAConfig | None = None, seed0: int =
                 else [run_ga(cfg, seed=x) for x in seeds])
         row = {"muL": float(mu), "runs": runs}
         for name, vals in (("discovery", [r.discovery for r in recs]), ("adaptation", [r.adaptation for r in recs])):
-            ok = [v for v in vals if v is not None]
-            cens = len(vals) - len(ok)
-            if ok and cens * 2 <= len(vals):
-                med, lo, hi = bootstrap_median_ci(ok, sample_size, resamples)
-                row[name] = dict(median=med, ci_lo=lo, ci_hi=hi, censored=cens)
-            else:
-                row[name] = dict(median=None, ci_lo=None, ci_hi=None, censored=cens)
+            row[name] = censored_median_ci(vals, cfg.cutoff, sample_size, resamples)
         rows.append(row)
+    if out is not None:
+        write_sweep_json(out, rows, base, seed0=seed0, sample_size=sample_size, resamples=resamples)
     return rows
+
+
+def write_sweep_json(path: str, rows: list[dict], cfg: GAConfig, **extra) -> None:
+    """Sweep JSON artefact: the per-muL rows plus the run configuration."""
+    import json
+    conf = {k: v for k, v in cfg.__dict__.items() if k not in ("init", "mu_L")}
+    conf["init"] = "all-zero" if cfg.init is None else "explicit"
+    with open(path, "w") as f:
+        json.dump({"config": conf, **extra, "points": rows}, f, indent=1)
+        f.write("\n")
+
+
+def write_trace_csv(record: RunRecord, path_or_buf=None) -> str:
+    """Optional per-run CSV trace: ``generation,best,mean,count_at_target``."""
+    import io
+    buf = io.StringIO()
+    buf.write("generation,best,mean,count_at_target\n")
+    for g in range(record.generations):
+        buf.write(f"{g},{int(record.best[g])},{float(record.mean[g])!r},{int(record.count_at_target[g])}\n")
+    text = buf.getvalue()
+    if path_or_buf is not None:
+        if hasattr(path_or_buf, "write"):
+            path_or_buf.write(text)
+        else:
+            with open(path_or_buf, "w") as f:
+                f.write(text)
+    return text

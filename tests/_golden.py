@@ -83,3 +83,19 @@ def histogram_from_outputs(out: dict, idx: np.ndarray, ks, hist_k) -> dict:
     np.minimum.at(rep_det, inv[isdet], ii[isdet])
     del spec
     return dict(keys=keys, det=det, steric=ste, rep_det=rep_det, rep_any=rep_any, tallies=tallies)
+
+
+def s32_sample(kind: str) -> tuple[np.ndarray, dict]:
+    """Indices and reference digests of the reference-pinned S32 samples
+    (tests/golden/make_s32_sample.py): 'blocks' = bench.py's 64 x 2^16 blocks,
+    'random' = 2^22 uniformly random indices (unique, sorted)."""
+    with open(os.path.join(GOLDEN, "s32_sample_digests.json")) as f:
+        meta = json.load(f)[kind]
+    if kind == "blocks":
+        s = meta["sample"]
+        idx = (np.arange(s["blocks"], dtype=np.uint64)[:, None] * np.uint64(s["stride"])
+               + np.arange(s["block"], dtype=np.uint64)[None, :]).reshape(-1)
+    else:
+        idx = np.unique(np.random.default_rng(32).integers(0, 1 << 32, 1 << 22, dtype=np.uint64))
+        assert idx.shape[0] == meta["sample"]["n"]
+    return idx, meta

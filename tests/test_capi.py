@@ -59,3 +59,30 @@ def test_argument_validation_is_host_side():
     with pytest.raises(TypeError):
         _kernels.classify_batch(np.arange(n, dtype=np.uint64), 2, 3, [], [], np.arange(23, -1, -1), 19, [8], 8, 0,
                                 True, outs[0].astype(np.int8), *outs[1:])
+
+
+def test_enumeration_rejects_indices_past_the_space():
+    """Index bits >= nfree are ignored by the decoder, so a range past 2^nfree would alias
+    genomes (idx mod 2^nfree) and count them twice: rejected before any device work."""
+    from paper_2205_15311_b200 import _lib
+    from paper_2205_15311_b200.classify import enumerate_space
+    from paper_2205_15311_b200.genome import SearchSpace
+    _lib_path()
+    L = _lib.lib()
+    a, bpl, mp, mv, fp = SearchSpace(2, 8).kernel_args()
+    ks = np.array([8], np.int64)
+    P = _lib.ptr
+    for start, count in (((1 << 24) - 10, 11), (1 << 24, 1), (2 ** 64 - 2, 5)):
+        rc = L.tv_enumerate_range(start, count, a, bpl, P(mp), P(mv), mp.shape[0], P(fp), fp.shape[0], 19, P(ks), 1,
+                                  8, 0, 1, None, None)
+        assert rc == -1 and (b"outside the space" in L.tv_last_error() or b"wraps" in L.tv_last_error())
+    # chunks: 3 chunks of 2^20 at stride 2^23 from 2^20 end at 2^20 + 2 * 2^23 + 2^20 > 2^24
+    rc = L.tv_enumerate_chunks(1 << 20, 3 << 20, 1 << 20, 1 << 23, a, bpl, P(mp), P(mv), mp.shape[0], P(fp),
+                               fp.shape[0], 19, P(ks), 1, 8, 0, 1, None, None)
+    assert rc == -1 and b"outside the space" in L.tv_last_error()
+    # in range: fails later, on the null histogram, not on the range
+    rc = L.tv_enumerate_chunks(0, 2 << 20, 1 << 20, 1 << 23, a, bpl, P(mp), P(mv), mp.shape[0], P(fp), fp.shape[0],
+                               19, P(ks), 1, 8, 0, 1, None, None)
+    assert rc == -1 and b"null histogram" in L.tv_last_error()
+    with pytest.raises(ValueError):
+        enumerate_space(SearchSpace(2, 8), ks=(8,), start=(1 << 24) - 10, count=20)

@@ -1,7 +1,9 @@
-"""Multi-rank histogram exchange over gloo (world size 2, CPU): the same
-allreduce_histogram code the NCCL path runs.  Each rank aggregates the
-reference's golden per-genome rows of ITS round-robin chunks; the exchanged
-result must equal the histogram of the whole slice on every rank."""
+"""Multi-rank histogram exchange over gloo (world sizes 2 and 4, CPU): the key-partitioned
+exchange (owner = hash mod R, all_to_all, owner-side merge, all_gather of the disjoint
+shards) that the NCCL path runs with a device-side merge.  Each rank aggregates the
+reference's golden per-genome rows of ITS round-robin chunks; the exchanged result must
+equal the histogram of the whole slice on every rank, and the owned shards must
+partition it."""
 import os
 import socket
 
@@ -34,7 +36,7 @@ def _worker(rank, world, port, name, chunk, q):
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
     from paper_2205_15311_b200.classify import chunk_plan
-    from paper_2205_15311_b200.distributed import allreduce_histogram, rank_chunks
+    from paper_2205_15311_b200.distributed import allreduce_histogram, owner_of, rank_chunks
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     try:
         c = G.slice_case(name)
@@ -43,28 +45,40 @@ def _worker(rank, world, port, name, chunk, q):
         rows = np.concatenate([np.arange(s, s + k) for s, k in mine]) if mine else np.zeros(0, np.int64)
         local = _hist_of(c, rows)
         merged = allreduce_histogram(local, None)
+        shard = allreduce_histogram(local, None, sharded=True)
         full = _hist_of(c, np.arange(n))
         ok = merged == full
-        q.put((rank, ok, len(merged), merged.total))
+        own = np.nonzero(owner_of(full.keys.astype(np.int64), world) == rank)[0]
+        shard_ok = (np.array_equal(shard.keys, full.keys[own]) and np.array_equal(shard.shape, full.shape[own])
+                    and np.array_equal(shard.rep_any, full.rep_any[own]) and np.array_equal(shard.det, full.det[own])
+                    and np.array_equal(shard.tallies, full.tallies))
+        q.put((rank, bool(ok) and bool(shard_ok), len(merged), merged.total, bool(ok), bool(shard_ok)))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,chunk", [("s28_800000", 256), ("s32_rand", 1000), ("s28_rand_k32", 100)])
-def test_allreduce_histogram_gloo_world2(name, chunk):
+def _spawn(target, world, *args):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, chunk, q)) for r in range(2)]
+    procs = [ctx.Process(target=target, args=(r, world, port, *args, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=180) for _ in procs]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, ok, nkeys, total in res:
-        assert ok, (rank, nkeys, total)
-    assert res[0][2:] == res[1][2:]
+    return res
+
+
+@pytest.mark.parametrize("name,chunk,world", [("s28_800000", 256, 2), ("s32_rand", 1000, 2), ("s28_rand_k32", 100, 2),
+                                              ("s28_800000", 300, 4), ("s28_rand", 20000, 4)])
+def test_allreduce_histogram_gloo(name, chunk, world):
+    """world 4 with 20000-index chunks of s28_rand: some ranks hold no genomes at all."""
+    res = _spawn(_worker, world, name, chunk)
+    for rank, ok, nkeys, total, *detail in res:
+        assert ok, (rank, nkeys, total, detail)
+    assert len({r[2:4] for r in res}) == 1
 
 
 def test_rank_chunks_partition():
@@ -136,15 +150,6 @@ def _collision_worker(rank, world, port, q):
 
 
 def test_allreduce_payload_from_representative_rank():
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_collision_worker, args=(r, 2, port, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    res = [q.get(timeout=180) for _ in procs]
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    res = _spawn(_collision_worker, 2)
     for r in res:
         assert r[1:] == (7, 1, 3, 3, 7), r

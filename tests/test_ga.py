@@ -131,6 +131,42 @@ def test_bootstrap_examples():
         E.bootstrap_median_ci([], 10, 10)
 
 
+def test_censored_median_rule_spec_448():
+    """censored runs stay in the median / bootstrap (as >= cutoff) unless > 50 % are censored."""
+    vals = [10, 20, 30, None, None]  # 40 % censored: they rank above every uncensored time
+    r = E.censored_median_ci(vals, 100, 5, 200)
+    assert r["median"] == 30.0 and r["censored"] == 2 and not r["median_censored"]
+    assert r["ci_hi"] == 100.0 and r["ci_hi_censored"]
+    # dropping the censored runs would have given 20 (the round-1 behaviour, biased low)
+    assert np.median([v for v in vals if v is not None]) == 20
+    r = E.censored_median_ci([5, None, None, 7, None, None], 100, 6, 200)
+    assert r["median"] is None and r["median_censored"] and r["censored"] == 4
+    r = E.censored_median_ci([1, None], 50, 2, 200)  # exactly half: kept, median straddles the cutoff
+    assert r["median"] == 25.5 and not r["median_censored"]
+    r = E.censored_median_ci([None, None, 3, None, 4, 5, None], 9, 7, 200)  # 4/7 > 50 %
+    assert r["median"] is None
+    r = E.censored_median_ci([None, 2, None, None, 4, 5], 9, 6, 200)  # 3/6: median (5 + 9) / 2, not censored
+    assert r["median"] == 7.0
+    r = E.censored_median_ci([None, None, 3, None], 9, 4, 200)  # 3/4 censored
+    assert r["median"] is None
+    with pytest.raises(ValueError):
+        E.censored_median_ci([], 10)
+
+
+def test_sweep_json_and_trace_csv(tmp_path):
+    import json
+    rows = [{"muL": 0.3, "runs": 2, "discovery": E.censored_median_ci([3, 4], 10, 2, 10),
+             "adaptation": E.censored_median_ci([None, 8], 10, 2, 10)}]
+    p = tmp_path / "sweep.json"
+    E.write_sweep_json(str(p), rows, E.GAConfig(), seed0=0)
+    doc = json.loads(p.read_text())
+    assert doc["points"][0]["muL"] == 0.3 and doc["config"]["pop_size"] == 512 and doc["config"]["init"] == "all-zero"
+    assert set(doc["points"][0]["discovery"]) >= {"median", "ci_lo", "ci_hi", "censored"}
+    rec = E.RunRecord(np.array([3, 5], np.uint32), np.array([0.5, 1.25]), np.array([0, 2], np.uint32), 2, 1, None)
+    txt = E.write_trace_csv(rec)
+    assert txt.splitlines() == ["generation,best,mean,count_at_target", "0,3,0.5,0", "1,5,1.25,2"]
+
+
 # ---------------------------------------------------------------- device (gpu)
 @pytest.mark.gpu
 @pytest.mark.parametrize("n,L,mode,lam,stop", [(512, 32, 0, 0.3, 0), (4096 + 3, 32, 1, 1.0, 0), (1 << 16, 64, 2, 4.0, 0),
@@ -171,6 +207,34 @@ def test_fujiyama_regime_desk_scale():
     assert ok03 >= 20 and cens4 >= 20, (ok03, cens4)
     rows = E.sweep([0.1, 0.3], runs=25)  # SPEC:452 sweep rows through the device sweep
     assert [r["muL"] for r in rows] == [0.1, 0.3] and rows[1]["adaptation"]["median"] is not None
+
+
+@pytest.mark.gpu
+def test_spec_run_ga_examples_100_runs(tmp_path):
+    """SPEC:413 (N=512, L=32, muL=0.3: discovery before the cutoff in >= 95/100 runs) and
+    SPEC:414 (muL=8: adaptation cutoff-censored in >= 95/100 runs), through the sweep API."""
+    import json
+    out = tmp_path / "sweep.json"
+    rows = E.sweep([0.3, 8.0], runs=100, base=E.GAConfig(stop_when="adaptation"), out=str(out))
+    assert rows[0]["discovery"]["censored"] <= 5, rows[0]
+    assert rows[1]["adaptation"]["censored"] >= 95, rows[1]
+    assert rows[1]["adaptation"]["median"] is None  # > 50 % censored: the median is reported censored
+    assert json.loads(out.read_text())["points"] == json.loads(json.dumps(rows))
+    disc = [r.discovery for r in E.run_replicas(E.GAConfig(mu_L=0.3, stop_when="discovery"), range(100))]
+    assert sum(x is not None for x in disc) >= 95
+
+
+@pytest.mark.gpu
+def test_spec_discovery_le_adaptation_1000_runs():
+    """discovery <= adaptation on every uncensored run, over 1000 runs (4 regimes x 250)."""
+    n_unc = 0
+    for i, mu in enumerate((0.1, 0.3, 1.0, 4.0)):
+        for r in E.run_replicas(E.GAConfig(mu_L=mu), range(1000 * i, 1000 * i + 250)):
+            assert E.discovery_time(r) == r.discovery and E.adaptation_time(r) == r.adaptation
+            if r.adaptation is not None:
+                assert r.discovery is not None and r.discovery <= r.adaptation
+                n_unc += 1
+    assert n_unc >= 250, n_unc
 
 
 @pytest.mark.gpu

@@ -62,14 +62,34 @@ def test_checkpoint_resume_equals_uninterrupted(mods, tmp_path):
     sp = Gm.SearchSpace(2, 8)
     ck = os.path.join(tmp_path, "enum.ckpt")
     full = C.enumerate_space(sp, ks=(1, 2, 4, 8), start=0x800000, count=1 << 20, batch_size=1 << 17)
-    # run only the first 3 of 8 batches, checkpointing every batch
-    plan = C.chunk_plan(0x800000, 1 << 20, 1 << 17)
-    C.enumerate_space(sp, ks=(1, 2, 4, 8), start=0x800000, count=1 << 20, chunks=plan[:3], checkpoint=ck,
-                      checkpoint_every=1)
+    # interrupt the run during batch 4 of 8 (the checkpoint written after batch 3 survives)
+    class Stop(Exception):
+        pass
+
+    def stop_at_4(done, total):
+        if done == 4:
+            raise Stop
+
+    with pytest.raises(Stop):
+        C.enumerate_space(sp, ks=(1, 2, 4, 8), start=0x800000, count=1 << 20, batch_size=1 << 17, checkpoint=ck,
+                          checkpoint_every=1, progress=stop_at_4)
     _, extra = C.Histogram.load(ck)
-    assert extra["chunks_done"] == 3
+    assert extra["chunks_done"] == 3 and extra["chunks_total"] == 8
     resumed = C.enumerate_space(sp, ks=(1, 2, 4, 8), start=0x800000, count=1 << 20, batch_size=1 << 17, resume=ck)
     assert resumed == full
+    # a checkpoint only resumes the very same plan and space (no silent double counting)
+    for kw in (dict(batch_size=1 << 16), dict(count=1 << 19), dict(start=0x800000 + (1 << 17))):
+        args = dict(ks=(1, 2, 4, 8), start=0x800000, count=1 << 20, batch_size=1 << 17, resume=ck)
+        args.update(kw)
+        with pytest.raises(ValueError):
+            C.enumerate_space(sp, **args)
+    with pytest.raises(ValueError):
+        C.enumerate_space(sp, ks=(1, 2, 4, 8), seed=1, start=0x800000, count=1 << 20, batch_size=1 << 17, resume=ck)
+    with pytest.raises(ValueError):  # same a, b, d, seed: only the fixed mask differs
+        C.enumerate_space(Gm.SearchSpace(2, 8, ((0, 0),)), ks=(1, 2, 4, 8), start=0, count=1 << 20,
+                          batch_size=1 << 17, resume=ck)
+    with pytest.raises(ValueError):  # indices past the end of the space would alias
+        C.enumerate_space(sp, ks=(8,), start=(1 << 24) - 10, count=20)
     hg = G.hist_golden("s28_1m")
     assert np.array_equal(full.keys, hg["keys"]) and np.array_equal(full.tallies, hg["tallies"])
     txt = full.to_csv()

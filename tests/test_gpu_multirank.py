@@ -34,3 +34,19 @@ def test_bench_two_ranks_share_one_gpu():
     assert b["n_gpus"] == 2 and b["config"]["histogram_ok"] is True
     assert b["value"] > 0 and b["e2e"]["value"] > 0
     assert b["s32"]["n_gpus"] == 2 and b["s32"]["histogram_ok"] is True
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_device_exchange_with_idle_ranks(world):
+    """enumerate_space_distributed through the device-side, key-partitioned exchange, with ranks
+    that enumerate nothing (count < world * batch_size) but own keys whose payloads they must
+    re-derive (the enumeration parameters are registered on every rank), a ragged
+    range and an S32 block; every rank's merged histogram equals the single-GPU one."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "tests/_dist_enum_worker.py"]
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    res = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert sorted(r["rank"] for r in res) == list(range(world))
+    for r in res:
+        assert r["s28_idle"] and r["s28_ragged"] and r["s32_block"], r

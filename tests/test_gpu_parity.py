@@ -105,6 +105,27 @@ def test_large_slice_digests(K, name, args):
         assert G.sha(out[k]) == dg["digests"][k], (name, k)
 
 
+@pytest.mark.parametrize("kind", ["blocks", "random"])
+def test_s32_reference_samples(K, kind):
+    """S32 pinned directly to the REFERENCE (numba) at scale: 4.2 M genomes over the whole
+    2^32 index range (bench.py's 64 x 2^16 blocks; 2^22 random indices), every per-genome
+    output column by SHA-256, and the device histogram of the same indices vs the
+    reference aggregate (tests/golden/make_s32_sample.py)."""
+    from paper_2205_15311_b200.classify import DeviceHistogram
+    from paper_2205_15311_b200.genome import space_from_preset
+    idx, meta = G.s32_sample(kind)
+    out = G.fresh_outputs(idx.shape[0], 1)
+    K.classify_batch(idx, *S32_ARGS, 19, np.array([7]), 7, np.uint64(0), True, *[out[k] for k in G.OUT_KEYS])
+    for k in G.OUT_KEYS:
+        assert G.sha(out[k]) == meta["digests"][k], (kind, k)
+    dev = DeviceHistogram((7,), 7, 5, 1 << 16)
+    dev.enumerate_indices(space_from_preset("s32_3_8"), idx[::-1].copy(), 19, 0, True)  # any order
+    h = dev.export()
+    dev.close()
+    _check_hist(h, "s32_" + kind)
+    assert len(h) == meta["n_keys"]
+
+
 def test_random_s32_vs_oracle(K):
     """2^20 random S32 indices, GPU vs the pinned oracle (all host threads)."""
     from oracle import oracle as O

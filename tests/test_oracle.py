@@ -105,3 +105,20 @@ def test_full_s28_digests():
                      np.array([1, 2, 4, 8]), 8, 0, True, *[out[k] for k in G.OUT_KEYS])
     for k in G.OUT_KEYS:
         assert G.sha(out[k]) == dg["digests"][k], k
+
+
+@pytest.mark.parametrize("kind", ["blocks", "random"])
+def test_s32_reference_samples(kind):
+    """The oracle equals the REFERENCE (numba) on 4.2 M S32 genomes spread over the whole
+    2^32 index range (tests/golden/make_s32_sample.py): every output column's digest and
+    the histogram aggregate."""
+    idx, meta = G.s32_sample(kind)
+    a, bpl, mp, mv, free = 3, 3, np.array([32, 33, 34, 35]), np.zeros(4, np.uint8), np.arange(31, -1, -1)
+    out = G.fresh_outputs(idx.shape[0], 1)
+    O.classify_batch(idx, a, bpl, mp, mv, free, 19, np.array([7]), 7, 0, True, *[out[k] for k in G.OUT_KEYS])
+    for k in G.OUT_KEYS:
+        assert G.sha(out[k]) == meta["digests"][k], (kind, k)
+    hg = G.hist_golden("s32_" + kind)
+    mine = G.histogram_from_outputs(out, idx, [7], 7)
+    for k in ("keys", "det", "steric", "rep_det", "rep_any", "tallies"):
+        assert np.array_equal(mine[k].astype(np.int64), hg[k].astype(np.int64)), k
