@@ -123,6 +123,9 @@ int tv_hist_export(tv_hist *h, int64_t max_records, uint32_t *keys, uint64_t *de
                    uint64_t *shape, int64_t *tallies, int64_t *n_out, void *stream);
 /* Merge records (same layout as export, [h|d]) and tallies (host, may be NULL)
  * into h: counts add, representatives take the minimum. */
+int tv_hist_merge(tv_hist *h, int64_t n, const uint32_t *keys, const uint64_t *det, const uint64_t *steric,
+                  const uint64_t *rep_det, const uint64_t *rep_any, const uint8_t *w, const uint8_t *hh,
+                  const uint16_t *cells, const uint64_t *shape, const int64_t *tallies, void *stream);
 /* Multi-GPU exchange (device-resident, no payload fix-up on the way): pack the raw
  * records as rows {key, det, steric, rep_det, rep_any, pay_idx, whc, shape[W]}
  * (7 + W u64 each; pay_idx = the genome whose payload the row carries) and the
@@ -133,9 +136,6 @@ int tv_hist_export(tv_hist *h, int64_t max_records, uint32_t *keys, uint64_t *de
 int tv_hist_pack(tv_hist *h, int64_t max_records, uint64_t *rows, int64_t *tallies, int64_t *n_out,
                  void *stream);
 int tv_hist_replace_rows(tv_hist *h, int64_t n, const uint64_t *rows, const int64_t *tallies, void *stream);
-int tv_hist_merge(tv_hist *h, int64_t n, const uint32_t *keys, const uint64_t *det, const uint64_t *steric,
-                  const uint64_t *rep_det, const uint64_t *rep_any, const uint8_t *w, const uint8_t *hh,
-                  const uint16_t *cells, const uint64_t *shape, const int64_t *tallies, void *stream);
 
 /* Fused enumerate -> classify -> histogram over indices [start, start+count)
  * of a space (same space arguments as tv_classify_batch).  No per-genome
@@ -176,6 +176,9 @@ int tv_ga_population_ptr(tv_ga *h, uint64_t **dev_ptr);
  * stats best/sum/count(f >= target) [h|d] (may be NULL), stop after recording
  * a generation with count >= 1 (stop_when 1) or >= adapt_count (2), else
  * reproduce.  *gens_done = generations evaluated.  Synchronises. */
+int tv_ga_run(tv_ga *h, uint64_t seed, int64_t g0, int64_t n_gens, uint32_t target, int64_t adapt_count,
+              int32_t stop_when, const uint32_t *f_ext, uint32_t *best, uint64_t *sum, uint32_t *count,
+              int64_t *gens_done, void *stream);
 /* R independent GA runs (SPEC.md:415-432 sweeps) in one launch, one CTA per run with
  * the population in shared memory (n <= 8192).  Run r is bit-identical to
  * tv_ga_run with seed seeds[r] from the same initial population (init [h|d]
@@ -186,9 +189,6 @@ int tv_ga_replicas(int64_t n, int32_t L, int32_t mode, const uint64_t *T, int32_
                    const uint64_t *init, int64_t g0, int64_t n_gens, uint32_t target, int64_t adapt_count,
                    int32_t stop_when, int64_t *done, int64_t *disc, int64_t *adapt, uint32_t *best, uint64_t *sum,
                    uint32_t *count, uint64_t *final_pop, void *stream);
-int tv_ga_run(tv_ga *h, uint64_t seed, int64_t g0, int64_t n_gens, uint32_t target, int64_t adapt_count,
-              int32_t stop_when, const uint32_t *f_ext, uint32_t *best, uint64_t *sum, uint32_t *count,
-              int64_t *gens_done, void *stream);
 /* JaTAM-shape fitness of the current population read as enumeration indices of
  * the space: f = d^2 - shapediff(target, run-0 grid) if DET at k, else 0.
  * target_occ u8[d*d] host (seed-centred board); f_out device u32[n]. */
