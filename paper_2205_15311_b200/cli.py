@@ -208,14 +208,28 @@ def _svg(shape, title: str, cell: int = 16) -> str:
     return "\n".join(out) + "\n"
 
 
-def _render_one(space, g: Genome, args, genome_index: int | None = None) -> str:
+def _render_one(space, g: Genome, args, want_hash: int | None = None) -> str:
     from . import assembly as A
     from .classify import crop, shape_hash
 
     tiles = decode_tileset(g, space)
-    gi = index_of_genome(space, g) if genome_index is None else genome_index
+    gi = index_of_genome(space, g)
     strict = not args.no_strict
-    if args.k is None:
+    if want_hash is not None:
+        # atlas row: the representative may be STERIC (rep = lowest DET-or-STERIC index), so draw
+        # the first of its k runs that assembles the row's shape (the run _k:351-381 attributes)
+        kind = A.classify_tileset(tiles, args.grid, args.k, seed=args.seed, genome_index=gi,
+                                  strict_contacts=strict).kind.name
+        for run in range(args.k):
+            o = A.assemble_once(tiles, args.grid, seed=args.seed, genome_index=gi, run_index=run,
+                                strict_contacts=strict)
+            if o.grid is not None and shape_hash(crop(o.grid)) == want_hash:
+                shape = crop(o.grid)
+                break
+        else:
+            raise CliError(f"{g.to_text()}: no run assembles shape 0x{want_hash:08x} (histogram from other "
+                           "parameters?)")
+    elif args.k is None:
         o = A.assemble_once(tiles, args.grid, seed=args.seed, genome_index=gi, run_index=0, strict_contacts=strict)
         kind, shape = o.kind.name, (crop(o.grid) if o.grid is not None else None)
     else:
@@ -260,7 +274,7 @@ def cmd_render(args) -> int:
             g = _parse_genome(r["representative_genome"], space)
             parts.append(f"# det_count={r['det_count']} steric_count={r['steric_count']} "
                          f"csv_hash={r['hash_hex']}\n" if args.format == "ascii" else "")
-            parts.append(_render_one(space, g, args))
+            parts.append(_render_one(space, g, args, want_hash=int(r["hash_hex"], 16)))
     text = "".join(parts)
     if args.out:
         _check_writable(args.out)

@@ -182,6 +182,9 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
     const char *eth = getenv("TV_FAST_THREADS");
     // parked lanes that trigger a service pass (measured: a = 2 best at 12, a = 3 at 20)
     P.service_thresh = et ? atoi(et) : (P.a == 3 ? 20 : 12);
+    // locally-forced run-0 assemblies end the genome DET after one run (TV_FORCED=0 disables)
+    const char *efz = getenv("TV_FORCED");
+    P.forced_check = efz ? (atoi(efz) != 0) : 1;
     // per-CTA phenotype cache: 256 slots (with the behaviour-sorted order a CTA sees many
     // phenotypes of alike genomes: S28 32.3 -> 31.6 ms vs 128 slots; 512 halves occupancy)
     P.cta_slots = P.hist_mode ? (ec ? atoi(ec) : 256) : 0;
@@ -218,25 +221,30 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
       const int64_t warps = blocks * (threads / 32);
       CK(S.get(&P.spill, (size_t)std::max(1, P.spill_cap) * 32 * warps));
       CK(S.get(&P.run_hash, (size_t)P.kmax * 32 * warps));
-      // early unbound cut-off: per-genome trivial-freedom bits from a full-SIMT pre-pass.
-      // Default on for a <= 2 (full S_{2,8}: 39.4 -> 38.9 ms incl. the 1.1 ms pre-pass);
-      // off for a = 3, where the 12-candidate proof costs more than it saves (S32
-      // 2^24 block: 42.7 -> 45.5 ms).  TV_EARLY_UNBOUND=0/1 forces it off/on.
+      // early unbound cut-off: per-genome trivial-freedom bits from a full-SIMT pre-pass
+      // (fixpoint proof, CandSwar::trivial_free).  Full S_{2,8} 25.0 -> 18.8 ms, S32 2^24
+      // block 28.7 -> 24.4 ms (pre-pass 1.4 / 2.9 ms included).  TV_EARLY_UNBOUND=0/1 forces it.
       const char *eu = getenv("TV_EARLY_UNBOUND");
       const char *eo = getenv("TV_ORDER");
       // (payload and fitness modes stop at the first UNBOUND run anyway)
-      const bool want_flags = !P.pay_mode && !P.fit_mode && (eu ? atoi(eu) != 0 : P.a <= 2);
+      const bool want_flags = !P.pay_mode && !P.fit_mode && (eu ? atoi(eu) != 0 : true);
       // behaviour-sorted processing order for every mode (outputs stay addressed by item):
       // see k_prepass.  Classify-type calls above 2^30 items keep item order (sort scratch).
       // TV_ORDER=0 disables it.
       const bool want_order = (P.hist_mode || P.n <= ((int64_t)1 << 30)) && P.n >= 4096 && !P.pay_mode &&
                               (eo ? atoi(eo) != 0 : true);  // (payload-mode items are (record, run) pairs)
+      // 1-mers (seed faces bond nothing) classified by the pre-pass and sorted past the end of
+      // the fast kernel's work (k_prepass).  TV_ONEMER=0 disables it.
+      const char *e1 = getenv("TV_ONEMER");
+      const bool want_onemer = want_order && !P.fit_mode && (e1 ? atoi(e1) != 0 : true);
       // histogram mode runs in slices of <= 2^26 items (sort and flag scratch stay bounded;
       // the histogram accumulates across slices)
       const int64_t n_all = P.n, slice = P.hist_mode ? ((int64_t)1 << 26) : n_all;
       const int64_t smax = std::min(n_all, slice);
       uint32_t *flags = nullptr, *order = nullptr, *iota = nullptr;
       uint16_t *key = nullptr, *key_sorted = nullptr;
+      unsigned long long *n_skip = nullptr;
+      if (want_onemer) CK(S.get(&n_skip, 1));
       uint8_t *tmp = nullptr;
       size_t tmp_bytes = 0;
       const int64_t nwmax = (smax + 31) / 32;
@@ -257,13 +265,15 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
         P.n = std::min(slice, n_all - off);
         P.tf_flags = nullptr;
         P.order = nullptr;
+        P.n_skip = nullptr;
         if (off > 0) CK(cudaMemsetAsync(work, 0, sizeof(unsigned long long), st));
+        if (n_skip) CK(cudaMemsetAsync(n_skip, 0, sizeof(unsigned long long), st));
         if (want_flags || want_order) {
           const int64_t nw = (P.n + 31) / 32;
           const int64_t fb = std::min<int64_t>((nw * 32 + 255) / 256, (int64_t)nsm * 8);
           uint16_t *kk = want_order ? key : nullptr;
           uint32_t *ff_flags = want_flags ? flags : nullptr;
-          void *fargs[] = {&P, &ff_flags, &kk, &iota};
+          void *fargs[] = {&P, &ff_flags, &kk, &iota, &n_skip};
           CK(cudaLaunchKernel(ff, dim3((unsigned)fb), dim3(256), fargs, 0, st));
           if (want_order) {  // stable LSD radix sort of the items by their 10-bit behaviour key
             size_t tb = tmp_bytes;
@@ -271,6 +281,7 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
           }
           P.tf_flags = ff_flags;
           P.order = want_order ? order : nullptr;
+          P.n_skip = n_skip;
         }
         void *args[] = {&P};
         CK(cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(threads), args, smem, st));

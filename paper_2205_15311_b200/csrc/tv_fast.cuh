@@ -185,76 +185,108 @@ template <typename M, int NC, bool STRICT> struct CandSwar {
     return (nz_nib<M>(CLS ^ rep_nib<M>(get_nib<M>(CLS, cf))) & cand) != 0;
   }
 
+  // Locally-forced check for one placed tile (candidate v) of a finished BOUNDED assembly:
+  // the candidates that bond v's face toward its neighbour cell q (a one-neighbour context,
+  // no strict conflict possible) must all have q's in-situ code (q occupied, value qv < NC)
+  // or not exist (q empty).  Sides j = N, E, S, W of v; q sees v from side (j + 2) & 3.
+  __device__ __forceinline__ bool forced_at(uint32_t v, uint32_t qN, uint32_t qE, uint32_t qS, uint32_t qW) const {
+    const M H0 = eqn(P2, get_nib<M>(E0, v)), H1 = eqn(P3, get_nib<M>(E1, v));
+    const M H2 = eqn(P0, get_nib<M>(E2, v)), H3 = eqn(P1, get_nib<M>(E3, v));
+    const bool o0 = qN < NC ? !ambiguous(H0, qN) : H0 == 0, o1 = qE < NC ? !ambiguous(H1, qE) : H1 == 0;
+    const bool o2 = qS < NC ? !ambiguous(H2, qS) : H2 == 0, o3 = qW < NC ? !ambiguous(H3, qW) : H3 == 0;
+    return o0 && o1 && o2 && o3;
+  }
+
   // nibble c of X equals v -> bit 4c+3
   __device__ __forceinline__ static M eqn(M X, uint32_t v) { return ~nz_nib<M>(X ^ rep_nib<M>(v)) & VALID; }
 
   // Static proof that no run of this genome can end TRIVIAL (early unbound
   // cut-off).  Over-approximates what a popped cell can
-  // see: R = candidates ever placeable (closure from the seed, candidate 0,
-  // under "bonds a label some candidate of R shows toward it from that side"),
-  // and a context = at most one label per side shown by R (empty sides are
-  // always compatible).  A TRIVIAL needs two hits with different in-situ codes
-  // in one context (_k:199-209): pair (c1, c2) can co-hit iff one side bonds
-  // both (same partner label), or two different sides bond one each while the
-  // other candidate tolerates that label (strict: its face there is 0 or
-  // bonds it, _k:176-198).  No such pair -> TRIVIAL is impossible.
+  // see: S[k] = labels a placed tile can show toward a popped cell from side k,
+  // bond[c] = sides through which candidate c bonds a label of S.  A placed tile
+  // never shows a label toward a popped cell through a side it bonded at
+  // placement (that neighbour was occupied then, and cells never empty again),
+  // so candidate c contributes its face f = (k+2)&3 to S[k] only if it can bond
+  // through some side other than f; the seed (no bonded side) shows all four
+  // faces.  S and bond grow to a joint fixpoint.  A context = at most one label
+  // of S[k] per side k (empty sides are always compatible).  A TRIVIAL needs two
+  // hits with different in-situ codes in one context (_k:199-209): pair (c1, c2)
+  // can co-hit iff one side bonds both (same partner label), or two different
+  // sides bond one each while the other candidate tolerates that label (strict:
+  // its face there is 0 or bonds it, _k:176-198).  No such pair -> TRIVIAL is
+  // impossible.  (Checked against the oracle on all of S_{2,8}: no genome it
+  // proves goes TRIVIAL; tools/work_analysis.c.)
+  //
+  // Byte-SWAR over the four sides (byte k <-> side k): S = labels shown from each side (bit
+  // per label), PM[c] = c's partner label per side (one-hot; faces 0 and 7 bond nothing),
+  // FM[c] = the label c shows, as a tile at side k of a popped cell, toward that cell (its
+  // face (k+2)&3), FC[c] = c's four faces.  ~10 int ops per candidate per
+  // fixpoint round; the pair test compares byte-packed faces (equal faces <=> equal
+  // in-situ codes, and <=> equal partners since the partner map is injective).
+  __device__ __forceinline__ static uint32_t nz_byte(uint32_t x) {  // bit 8k+7 set iff byte k != 0
+    return (((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u;
+  }
   __device__ __forceinline__ bool trivial_free() const {
-    const M E[4] = {E0, E1, E2, E3}, Pt[4] = {P0, P1, P2, P3};
-    M U[NC];  // U[c2]: candidates c that show c2's partner label on some side facing c2
+    uint32_t PM[NC], FM[NC];
 #pragma unroll
-    for (int c2 = 0; c2 < NC; c2++) {
-      U[c2] = 0;
-#pragma unroll
-      for (int k = 0; k < 4; k++) U[c2] |= eqn(E[(k + 2) & 3], get_nib<M>(Pt[k], c2));
+    for (int c = 0; c < NC; c++) {
+      const uint32_t e0 = get_nib<M>(E0, c), e1 = get_nib<M>(E1, c), e2 = get_nib<M>(E2, c), e3 = get_nib<M>(E3, c);
+      FM[c] = (1u << e2) | ((1u << e3) << 8) | ((1u << e0) << 16) | ((1u << e1) << 24);
+      PM[c] = ((1u << get_nib<M>(P0, c)) & 0xFEu) | (((1u << get_nib<M>(P1, c)) & 0xFEu) << 8) |
+              (((1u << get_nib<M>(P2, c)) & 0xFEu) << 16) | (((1u << get_nib<M>(P3, c)) & 0xFEu) << 24);
     }
-    M Rn = (M)8;  // candidate 0 (the seed) in nibble-flag form
+    uint32_t S = FM[0];  // the seed (no bonded side) shows all four faces
 #pragma unroll 1
-    for (int it = 0; it < NC; it++) {
-      M R2 = Rn;
+    for (int it = 0; it < 32; it++) {
+      uint32_t S2 = S;
 #pragma unroll
-      for (int c2 = 0; c2 < NC; c2++) R2 |= (U[c2] & Rn) ? ((M)8 << (4 * c2)) : (M)0;
-      if (R2 == Rn) break;
-      Rn = R2;
-    }
-    // S[k]: labels a placeable candidate can show toward a cell from side k (bit per label)
-    uint32_t S[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-    for (int c = 0; c < NC; c++) {
-      const uint32_t in = (uint32_t)((Rn >> (4 * c + 3)) & 1u);
-#pragma unroll
-      for (int k = 0; k < 4; k++) S[k] |= in << get_nib<M>(E[(k + 2) & 3], c);
-    }
-    // per candidate, nibble-flag form (bit 4k+3 <-> side k): sides that can bond it, zero faces;
-    // packed partner labels (the partner map is injective, so equal packs <=> equal codes, _k:199)
-    uint32_t bond[NC], z[NC], pc[NC];
-#pragma unroll
-    for (int c = 0; c < NC; c++) {
-      bond[c] = 0u; z[c] = 0u; pc[c] = 0u;
-#pragma unroll
-      for (int k = 0; k < 4; k++) {
-        const uint32_t pk = get_nib<M>(Pt[k], c);
-        bond[c] |= ((S[k] >> pk) & 1u) << (4 * k + 3);  // partner 15 (face 0) is never shown
-        pc[c] |= pk << (4 * k);
+      for (int c = 0; c < NC; c++) {
+        const uint32_t nzb = nz_byte(PM[c] & S);  // sides through which c can bond
+        const uint32_t excl = (nzb & (nzb - 1u)) == 0u ? __funnelshift_l(nzb, nzb, 16) : 0u;
+        S2 |= nzb ? FM[c] & ~((excl >> 7) * 0xFFu) : 0u;
       }
-      z[c] = ~nz_nib<uint32_t>((uint32_t)(((E0 >> (4 * c)) & 15u) | (((E1 >> (4 * c)) & 15u) << 4) |
-                                          (((E2 >> (4 * c)) & 15u) << 8) | (((E3 >> (4 * c)) & 15u) << 12))) &
-             0x8888u;
+      if (S2 == S) break;
+      S = S2;
     }
-    bool ok = true;
+    // pair test, SWAR over c2 for each c1 (nibble flags bit 4c+3): BK[k] = candidates that
+    // bond through side k, ZK[k] = zero face at side k, SK = same face as c1 at side k
+    M BK[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int c = 0; c < NC; c++) {
+      const uint32_t b = nz_byte(PM[c] & S);
+#pragma unroll
+      for (int k = 0; k < 4; k++) BK[k] |= (M)((b >> (8 * k + 7)) & 1u) << (4 * c + 3);
+    }
+    const M E[4] = {E0, E1, E2, E3};
+    M bad = 0;
 #pragma unroll
     for (int c1 = 0; c1 < NC; c1++) {
+      M SK[4], A = 0, tol2 = 0, bnd2 = 0;
+      uint32_t nb1 = 0;  // sides c1 bonds through (bit k)
 #pragma unroll
-      for (int c2 = c1 + 1; c2 < NC; c2++) {
-        const uint32_t same = ~nz_nib<uint32_t>(pc[c1] ^ pc[c2]) & 0x8888u;  // same partner label per side
-        const uint32_t b1 = bond[c1] & (STRICT ? (same | z[c2]) : 0x8888u);
-        const uint32_t b2 = bond[c2] & (STRICT ? (same | z[c1]) : 0x8888u);
-        // strict: b1 == b2 == one side k forces k into `same` (else both faces at k are 0 and
-        // neither bonds there), so the single-side exclusion only matters without the rule
-        const bool pair = (bond[c1] & same) != 0u ||
-                          (STRICT ? (b1 && b2) : (b1 && b2 && !(b1 == b2 && (b1 & (b1 - 1u)) == 0u)));
-        ok = ok && !(pair && pc[c1] != pc[c2]);  // equal partner codes <=> equal in-situ codes
+      for (int k = 0; k < 4; k++) {
+        const uint32_t ek = get_nib<M>(E[k], c1);
+        SK[k] = eqn(E[k], ek);
+        const bool b1k = ((BK[k] >> (4 * c1 + 3)) & 1u) != 0;
+        nb1 |= (uint32_t)b1k << k;
+        A |= b1k ? SK[k] : (M)0;                               // one side bonds both
+        if (STRICT) {
+          tol2 |= b1k ? (SK[k] | (~nz_nib<M>(E[k]) & VALID)) : (M)0;  // c2 tolerates c1's bond side
+          bnd2 |= BK[k] & (ek == 0u ? VALID : SK[k]);         // c2 bonds where c1 tolerates
+        }
       }
+      if (!STRICT) {  // c1 bonds k1, c2 bonds some k2 != k1 (no tolerance needed)
+        const bool single = (nb1 & (nb1 - 1u)) == 0u;
+        M other = 0;
+#pragma unroll
+        for (int k = 0; k < 4; k++) other |= (single && ((nb1 >> k) & 1u)) ? (M)0 : BK[k];
+        tol2 = nb1 ? VALID : (M)0;
+        bnd2 = other;
+      }
+      const M differ = ~(SK[0] & SK[1] & SK[2] & SK[3]) & VALID;  // different in-situ code
+      bad |= (A | (tol2 & bnd2)) & differ;
     }
+    const bool ok = bad == 0;
     return ok;
   }
 };
@@ -274,7 +306,7 @@ __host__ __device__ inline int fast_board_words(int a, int d) {
 #define TV_KEY_BITS 11  // width of the k_prepass behaviour key
 
 #ifndef TV_PREPASS_MINB
-#define TV_PREPASS_MINB 3  // k_prepass at <= 80 registers (3 CTAs of 256 per SM)
+#define TV_PREPASS_MINB 2  // k_prepass at <= 128 registers (2 CTAs of 256 per SM; the fixpoint proof spills at 80)
 #endif
 #ifndef TV_FAST_MINB
 #define TV_FAST_MINB 2
@@ -330,6 +362,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
   const int cr = (d >> 1) + 1, centre = cr * RS + cr;
   const int thresh = P.service_thresh > 0 ? P.service_thresh : 16;
 
+  const int64_t n_run = P.n - (P.n_skip ? (int64_t)*P.n_skip : 0);  // 1-mers classified by k_prepass
   int st = ST_NEED, pend = -1;
   int64_t item = 0;
   uint64_t idx = 0, rs = 0;
@@ -356,6 +389,8 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
         uint32_t hs = 0;
         int w = 0, h = 0, n = 0, ov = 0;
         const bool fit_scan = P.fit_mode && !replay && run == 0;  // overlap with the GA target shape
+        // run 0 of a genome: is its assembly locally forced (every run must reproduce it)?
+        bool forced = P.forced_check && !replay && !P.pay_mode && run == 0;
         if (ended == RUN_BOUNDED) {
           unsigned long long *out = nullptr;
           int64_t W = 0;
@@ -380,6 +415,9 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
               const int y = (int)R - minr, x = col - minc;
               hs = oat_step(oat_step(hs, (uint32_t)x), (uint32_t)y);
               n++;
+              if (forced)
+                forced = K.forced_at((Ln.gw[wi * 32] >> (b & ~3)) & 15u, Ln.nib((int)L - RS), Ln.nib((int)L + 1),
+                                     Ln.nib((int)L + RS), Ln.nib((int)L - 1));
               if (fit_scan) ov += (P.target_rows[R] >> col) & 1u;
               if (out) {
                 const int bit = y * w + x;
@@ -423,7 +461,12 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
           bool done = false;
           if (ended == RUN_BOUNDED) {
             rh[run * 32] = hs;
-            if (run == 0) { hash0 = hs; fit0 = (uint32_t)n | ((uint32_t)ov << 16); }
+            if (run == 0) {
+              hash0 = hs; fit0 = (uint32_t)n | ((uint32_t)ov << 16);
+              // locally forced: every later run assembles the same shape BOUNDED, so the
+              // genome is DET at every k with this hash
+              if (forced) done = true;
+            }
             else if (first_mismatch < 0 && first_unbound != 0 && hs != hash0) first_mismatch = run;
             if (P.fit_mode && first_mismatch >= 0) done = true;  // not DET: fitness 0 whatever follows
           } else if (ended == RUN_UNBOUND) {
@@ -541,7 +584,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
         base = __shfl_sync(0xFFFFFFFFu, base, leader);
         if (st == ST_NEED) {
           item = (int64_t)base + __popc(need & ((1u << lane) - 1u));
-          if (item >= P.n) {
+          if (item >= n_run) {
             st = ST_DONE;
           } else {
             // behaviour-sorted processing order (k_prepass); every per-item output and flag below
@@ -694,27 +737,39 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
 //    outcomes: fewer idle lanes.
 //    Results cannot depend on the order (per-genome substreams, commutative
 //    histogram updates).
+//  * 1-mers (with key): a genome whose seed faces bond no label of the genome gets
+//    no hit at any centre neighbour, so every run drops the four and ends BOUNDED
+//    with the 1x1 shape (_k:138-249): DET at every k, hash 0x3a9be4cf.  When
+//    n_skip is given the pre-pass classifies these itself (histogram: tallies,
+//    counts, representatives, payload; classify mode: the output rows), gives
+//    them the largest key so they sort to the end of the order, and counts them
+//    in *n_skip; k_classify_fast stops at n - *n_skip.
+constexpr uint32_t kOneMerHash = 0x3a9be4cfu;  // OAT of (w, h, x, y) = (1, 1, 0, 0), _k:260-277
+constexpr uint16_t kOneMerKey = (1u << TV_KEY_BITS) - 1u;
+
 template <int A, bool STRICT>
 __global__ void __launch_bounds__(256, TV_PREPASS_MINB) k_prepass(const __grid_constant__ ClassifyParams P, uint32_t *flags,
-                                                 uint16_t *key_out, uint32_t *iota_out) {
+                                                 uint16_t *key_out, uint32_t *iota_out,
+                                                 unsigned long long *n_skip) {
   constexpr int NC = 4 * A;
   const int64_t nw = (P.n + 31) >> 5;
   const int lane = threadIdx.x & 31;
+  __shared__ unsigned long long s_om_min;
+  __shared__ unsigned int s_om_cnt;
+  if (threadIdx.x == 0) { s_om_min = ~0ULL; s_om_cnt = 0u; }
+  __syncthreads();
   for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~(int64_t)31; base < nw * 32;
        base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t item = base + lane;
-    bool f = false;
+    bool f = false, om = false;
     const bool valid = item < P.n;
+    uint64_t idx = 0;
     if (valid) {
-      const uint64_t idx = item_index(P.indices, P.start, P.chunk, P.stride, P.item0 + item);
+      idx = item_index(P.indices, P.start, P.chunk, P.stride, P.item0 + item);
       uint32_t lab[12];
 #pragma unroll
       for (int te = 0; te < 12; te++) lab[te] = te < NC ? decode_label(P.dec, te, idx) : 0u;
-      if (flags) {
-        Cand<A, STRICT> K;
-        K.build_faces(lab);  // tiles >= A have all-zero faces: they never bond, so never pair
-        f = K.trivial_free();
-      }
+      uint32_t kk = 0;
       if (key_out) {
         // behaviour key (bonds, _k:90-93): line-prone (a tile bonds a copy of itself through
         // opposite faces), seed tile bonds itself, bondable faces of the seed, another tile
@@ -742,16 +797,63 @@ __global__ void __launch_bounds__(256, TV_PREPASS_MINB) k_prepass(const __grid_c
             for (int g = 4; g < NC; g++) selfr |= (g >> 2) == (te >> 2) && bonds((int)x, (int)lab[g]);
           }
         }
-        uint32_t kk = ((line ? 0u : 1u) << 9) | ((self0 ? 0u : 1u) << 8) | ((uint32_t)(4 - nb0) << 5) |
-                      ((selfr ? 0u : 1u) << 4) | (uint32_t)(8 - nbr);
-        kk = (kk << 1) | (f ? 0u : 1u);  // trivial-freedom (a <= 2) as the lowest key bit
-        key_out[item] = (uint16_t)kk;
+        kk = ((line ? 0u : 1u) << 9) | ((self0 ? 0u : 1u) << 8) | ((uint32_t)(4 - nb0) << 5) |
+             ((selfr ? 0u : 1u) << 4) | (uint32_t)(8 - nbr);
+        om = n_skip != nullptr && nb0 == 0;
+      }
+      if (flags && !om) {  // (1-mers never reach the fast kernel)
+        Cand<A, STRICT> K;
+        K.build_faces(lab);  // tiles >= A have all-zero faces: they never bond, so never pair
+        f = K.trivial_free();
+      }
+      if (key_out) {
+        kk = (kk << 1) | (f ? 0u : 1u);  // trivial-freedom as the lowest key bit
+        key_out[item] = om ? kOneMerKey : (uint16_t)kk;
         iota_out[item] = (uint32_t)item | (f ? 0x80000000u : 0u);  // items < 2^31; bit 31 = flag
+        if (om && !P.hist_mode) {  // classify_batch row of a DET 1x1 genome (_k:438-452)
+          for (int k = 0; k < P.q; k++) P.out_class[item * P.q + k] = (uint8_t)CLS_DET;
+          P.out_hash[item] = kOneMerHash;
+          P.out_w[item] = 1; P.out_h[item] = 1; P.out_cells[item] = 1;
+          for (int64_t wj = 0; wj < P.W; wj++) P.out_shape[item * P.W + wj] = wj == 0 ? 1ULL : 0ULL;
+        }
       }
     }
     if (flags) {
       const uint32_t w = __ballot_sync(0xFFFFFFFFu, f);
       if (lane == 0) flags[base >> 5] = w;
+    }
+    if (n_skip) {
+      const unsigned om_mask = __ballot_sync(0xFFFFFFFFu, om);
+      if (om_mask) {
+        unsigned long long m = om ? idx : ~0ULL;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const unsigned long long x = __shfl_xor_sync(0xFFFFFFFFu, m, o);
+          m = x < m ? x : m;
+        }
+        if (lane == 0) { atomicAdd(&s_om_cnt, (unsigned)__popc(om_mask)); atomicMin(&s_om_min, m); }
+      }
+    }
+  }
+  if (n_skip) {
+    __syncthreads();
+    if (threadIdx.x == 0 && s_om_cnt) {
+      atomicAdd(n_skip, (unsigned long long)s_om_cnt);
+      if (P.hist_mode) {
+        for (int k = 0; k < P.q; k++) atomicAdd(&P.hist.tallies[k * 5 + CLS_DET], (unsigned long long)s_om_cnt);
+        bool gnew = false;
+        const int64_t g = hist_claim(P.hist, kOneMerHash, gnew);
+        if (g >= 0) {
+          atomicAdd(&P.hist.det[g], (unsigned long long)s_om_cnt);
+          hist_min(&P.hist.rep_det[g], s_om_min);
+          hist_min(&P.hist.rep_any[g], s_om_min);
+          if (gnew) {  // this CTA's lowest 1-mer provides the payload (fixed at export if another is lower)
+            P.hist.whc[g] = 1u | (1u << 8) | (1u << 16);
+            for (int wj = 0; wj < P.hist.W; wj++) P.hist.shape[g * P.hist.W + wj] = wj == 0 ? 1ULL : 0ULL;
+            P.hist.pay_idx[g] = s_om_min;
+          }
+        }
+      }
     }
   }
 }

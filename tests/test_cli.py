@@ -226,7 +226,8 @@ def test_render_atlas_from_histogram(tmp_path, capsys):
     assert len(blocks) == min(5, len(rows))
     for r, b in zip(rows, blocks):
         lines = b.splitlines()
-        assert f"csv_hash={r['hash_hex']}" in lines[0] and "DETERMINISTIC" in lines[1]
+        # the representative may classify STERIC; the drawn run is the one that assembles the row's shape
+        assert f"csv_hash={r['hash_hex']}" in lines[0] and f"hash={r['hash_hex']}" in lines[1]
         bm = np.array([[c == "#" for c in ln] for ln in lines[2:]], bool)
         s = CroppedShape(bm.shape[1], bm.shape[0], bm)
         assert f"0x{shape_hash(s):08x}" == r["hash_hex"]  # the drawn shape is the CSV row's shape

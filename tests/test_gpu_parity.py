@@ -180,18 +180,25 @@ def test_enumerate_generic_path_histogram(K):
         assert np.array_equal(getattr(h, k).astype(np.int64), exp[k].astype(np.int64)), k
 
 
+# Exact work elimination switches (read per launch): TV_EARLY_UNBOUND (stop at the first
+# UNBOUND run of a provably trivial-free genome), TV_ONEMER (1-mers classified by the
+# pre-pass), TV_FORCED (stop after run 0 when its assembly is locally forced).  Results must
+# be identical under every combination.
+SWITCHES = [(0, 0, 0), (1, 1, 1), (1, 0, 0), (0, 1, 0), (0, 0, 1)]
+
+
 @pytest.fixture
 def early_unbound(monkeypatch):
-    """Force the early-unbound cut-off on/off (read per launch from TV_EARLY_UNBOUND)."""
-    def set_(on: bool):
-        monkeypatch.setenv("TV_EARLY_UNBOUND", "1" if on else "0")
+    def set_(sw):
+        for name, v in zip(("TV_EARLY_UNBOUND", "TV_ONEMER", "TV_FORCED"), sw):
+            monkeypatch.setenv(name, str(int(v)))
     return set_
 
 
-@pytest.mark.parametrize("on", [False, True])
+@pytest.mark.parametrize("on", SWITCHES)
 def test_early_unbound_cutoff_s28_full(K, early_unbound, on):
-    """The cut-off stops a genome at its first UNBOUND run only when no run can go
-    TRIVIAL; the full-S28 histogram must not change either way."""
+    """The cut-offs skip only runs that cannot change a genome's outcome; the full-S28
+    histogram must not change under any combination."""
     from paper_2205_15311_b200.classify import enumerate_space
     from paper_2205_15311_b200.genome import SearchSpace
     early_unbound(on)
@@ -199,9 +206,9 @@ def test_early_unbound_cutoff_s28_full(K, early_unbound, on):
     _check_hist(h, "s28_full")
 
 
-@pytest.mark.parametrize("on", [False, True])
+@pytest.mark.parametrize("on", SWITCHES)
 def test_early_unbound_cutoff_per_genome(K, early_unbound, on):
-    """Per-genome rows (every column, every prefix k) with the cut-off forced on/off,
+    """Per-genome rows (every column, every prefix k) under each switch combination,
     for a = 1, 2, 3 and non-strict contacts, against the pinned oracle."""
     from oracle import oracle as O
     early_unbound(on)
