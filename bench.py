@@ -180,6 +180,84 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+def int_peak_ops(stream) -> float:
+    """Measured int32 ALU peak of this GPU (ops/s): tv_int_peak_launch, best of 3."""
+    import torch
+    from paper_2205_15311_b200 import _lib
+    L = _lib.lib()
+    sp = _lib.ctypes.c_void_p(stream.cuda_stream)
+    nsm = _lib.ctypes.c_int32()
+    L.tv_sm_count(_lib.ctypes.byref(nsm))
+    peak = 0.0
+    for _ in range(3):
+        ops = _lib.ctypes.c_double()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        _lib.check(L.tv_int_peak_launch(1 << 16, nsm.value * 8, 256, sp, _lib.ctypes.byref(ops)))
+        s1.record(stream)
+        torch.cuda.synchronize()
+        peak = max(peak, ops.value / (s0.elapsed_time(s1) / 1e3))
+    return peak
+
+
+def event_counts(name: str) -> dict:
+    return json.load(open(os.path.join(ROOT, "profiles", "event_counts.json")))[name]
+
+
+def enum_roofline(kernel: str, genomes: float, ms: float, peak: float, counts: dict, covers: str,
+                  traffic=None) -> dict:
+    """int32-issue roofline of an enumeration launch: algorithmic ops = the reference's event-
+    weighted op count x genomes; executed = the runs the kernel still runs after
+    the exact work elimination, same weights."""
+    alg = counts["ops_per_genome"] * genomes / (ms / 1e3)
+    exe = counts.get("ops_per_genome_executed", counts["ops_per_genome"]) * genomes / (ms / 1e3)
+    return {"bound": "int32_alu", "achieved": alg / 1e12, "peak": peak / 1e12, "unit": "Tops/s", "frac": alg / peak,
+            "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read+write)", "kernel": kernel,
+            "kernel_ms": ms, "kernel_ms_covers": covers, "ops_per_genome": counts["ops_per_genome"],
+            "ops_per_genome_executed": counts.get("ops_per_genome_executed"),
+            "achieved_executed": exe / 1e12, "frac_executed": exe / peak,
+            "peak_source": "measured on this GPU: tv_int_peak_launch (8 independent IADD3/LOP3 chains/thread)",
+            "ops_source": "event-weighted algorithmic int32 ops (SURVEY.md 8d weights) x oracle event counts, "
+                          "profiles/event_counts.json; *_executed counts only the runs the kernel executes"}
+
+
+def l2_ceilings(stream) -> dict:
+    """Measured L2 ceilings for the GA roofline: streaming read+write GB/s and random 16-byte
+    read GB/s over a 32 MiB L2-resident buffer, and the grid-barrier latency (us per grid.sync
+    at one 1024-thread CTA per SM)."""
+    import torch
+    from paper_2205_15311_b200 import _lib
+    L = _lib.lib()
+    sp = _lib.ctypes.c_void_p(stream.cuda_stream)
+    buf = torch.zeros(32 << 20, dtype=torch.uint8, device="cuda")
+    out = {}
+    for name, rnd in (("l2_stream_gbs", 0), ("l2_random16_gbs", 1)):
+        best = 0.0
+        for _ in range(3):
+            moved = _lib.ctypes.c_double()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            _lib.check(L.tv_l2_probe_launch(_lib.ctypes.c_void_p(buf.data_ptr()), buf.numel(), 8, rnd, sp,
+                                            _lib.ctypes.byref(moved)))
+            s1.record(stream)
+            torch.cuda.synchronize()
+            best = max(best, moved.value / (s0.elapsed_time(s1) / 1e3) / 1e9)
+        out[name] = best
+    times = []
+    for syncs in (0, 2000):
+        best = 1e9
+        for _ in range(3):
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            _lib.check(L.tv_gridsync_probe_launch(syncs, sp))
+            s1.record(stream)
+            torch.cuda.synchronize()
+            best = min(best, s0.elapsed_time(s1))
+        times.append(best)
+    out["grid_sync_us"] = (times[1] - times[0]) / 2000 * 1e3
+    return out
+
+
 def hbm_peak() -> float:
     try:
         return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
@@ -196,7 +274,7 @@ def ga_traffic():
         return None
 
 
-def ga_bench(args, n: int = 1 << 20, gens: int = 2000) -> dict:
+def ga_bench(args, n: int = 1 << 20, gens: int = 2000, ceil: dict | None = None) -> dict:
     """GA generations/s at population 2^20 (BASELINE.json configs[2]): Fujiyama, L=32,
     mu*L=0.3, asexual, no early stop; one cooperative launch per call."""
     import torch
@@ -237,13 +315,19 @@ def ga_bench(args, n: int = 1 << 20, gens: int = 2000) -> dict:
                          "frac": 16.0 * n * k / dev_s / 1e9 / hbm_peak(), "traffic": ga_traffic(),
                          "note": "16 B/individual/generation algorithmic (SURVEY 8d); working set L2-resident, so "
                                  "the binding limits are the two grid barriers per generation and dependent "
-                                 "L2 reads in selection (DESIGN.md section 6)"},
+                                 "L2 reads in selection (DESIGN.md section 6)",
+                         "l2": None if not ceil else {
+                             "measured": ceil, "source": "bench.py l2_ceilings(): tv_l2_probe_launch / "
+                                                         "tv_gridsync_probe_launch on this GPU",
+                             "frac_l2_stream": 16.0 * n * k / dev_s / 1e9 / ceil["l2_stream_gbs"],
+                             "barrier_floor_us_per_generation": 2 * ceil["grid_sync_us"],
+                             "frac_of_barrier_floor": 2 * ceil["grid_sync_us"] / (dev_s / k * 1e6)}},
             "cpu_baseline": {"value": cg / cpu_s, "unit": "generations/s", "cores": os.cpu_count(),
                              "kind": "restatement (no reference GA exists)",
                              "sample": f"{cg} generations of 2^20 on oracle/tv_ga_oracle.c, OpenMP"}}
 
 
-def s32_bench(args, rank: int, world: int, stream) -> dict:
+def s32_bench(args, rank: int, world: int, stream, peak: float | None = None) -> dict:
     """Full S^{32}_{3,8} (BASELINE.json configs[4]): all 2^32 indices, 2^24-index chunks dealt
     round-robin over the ranks, one histogram exchange; one timed pass after a warm-up chunk.
     Checked against the oracle's full-space tallies (tests/golden/hist_s32_full.json)."""
@@ -315,10 +399,14 @@ def s32_bench(args, rank: int, world: int, stream) -> dict:
             "config": {"workload": "full S^32_(3,8) enumeration: 2^32 genomes -> phenotype histogram", "ks": [7],
                        "hist_k": 7, "d": 19, "seed": 0, "strict": True, "chunking": f"{chunk} round-robin",
                        "timed": "one pass after a 2^24 warm-up chunk (inputs are index ranges; no L2 reuse)"},
-            "histogram_ok": ok, "phenotypes": len(final), "cpu_baseline": cpu}
+            "histogram_ok": ok, "phenotypes": len(final), "cpu_baseline": cpu,
+            "roofline": None if not peak else enum_roofline(
+                "k_classify_fast<3>", n_all / world, ms, peak, event_counts("s32_sample_2p22"),
+                "the whole timed pass: per 2^26-item slice k_prepass<3> + CUB radix sort + k_classify_fast<3> "
+                "(+ the exchange at N > 1); ops per genome from 64 evenly spaced 2^16 blocks")}
 
 
-def ga_jatam_bench(n: int = 1 << 20, gens: int = 20) -> dict:
+def ga_jatam_bench(n: int = 1 << 20, gens: int = 20, peak: float | None = None, cpu_leg: bool = True) -> dict:
     """GA with JaTAM-shape fitness (BASELINE.json configs[3]): population 2^20 of S_{2,8}
     genomes (L = 24), fitness = d^2 - shapediff(target, run-0 grid) for genomes DET at k = 8
     (k_classify_fast fit mode over the whole population each generation), then one GA
@@ -351,14 +439,47 @@ def ga_jatam_bench(n: int = 1 << 20, gens: int = 20) -> dict:
     e1.record(stream)
     torch.cuda.synchronize()
     dev_s = e0.elapsed_time(e1) / 1e3
+    pop_now = ga.population()
     ga.close()
+    cpu = None
+    if cpu_leg:
+        # CPU leg: the pinned C restatement classifies a 2^16 sample of the current population at
+        # k = 8 (the fitness needs the DET class and the run-0 shape) on all host threads, scaled
+        # to 2^20, plus one Fujiyama generation of the GA restatement at 2^20 (reproduction)
+        from oracle import oracle as O
+        a, bpl, mp, mv, fp = S28.kernel_args()
+        idx = np.ascontiguousarray(pop_now[: 1 << 16], np.uint64)
+        m = idx.shape[0]
+        outs = [np.zeros((m, 1), np.uint8), np.zeros(m, np.uint32), np.zeros(m, np.uint8), np.zeros(m, np.uint8),
+                np.zeros(m, np.uint16), np.zeros((m, 6), np.uint64)]
+        O.classify_batch(idx[:1024], a, bpl, mp, mv, fp, 19, np.array([8]), 8, 0, True, *[o[:1024] for o in outs])
+        t = time.perf_counter()
+        O.classify_batch(idx, a, bpl, mp, mv, fp, 19, np.array([8]), 8, 0, True, *outs)
+        t_cls = (time.perf_counter() - t) * (n / m)
+        pop = np.zeros(n, np.uint64)
+        t = time.perf_counter()
+        O.ga_run(pop, 24, 0, E.poisson_thresholds(0.3, 24), 5, 0, 1, 19 * 19, n, 0)
+        t_gen = time.perf_counter() - t
+        cpu = {"value": 1.0 / (t_cls + t_gen), "unit": "generations/s", "cores": os.cpu_count(),
+               "kind": "port (classification: pinned C restatement of the reference; reproduction: GA restatement)",
+               "sample": f"classify_batch k=8 of {m} genomes of the evolved population scaled x{n // m} "
+                         f"({t_cls:.2f} s per 2^20) + one 2^20 GA generation ({t_gen * 1e3:.0f} ms), OpenMP"}
+    roof = None
+    if peak:
+        roof = enum_roofline("k_classify_fast<2> (fit mode)", float(n), dev_s / gens * 1e3, peak,
+                             event_counts("s28_full"),
+                             "one GA generation: k_prepass + sort + k_classify_fast fit mode over 2^20 genomes + "
+                             "one k_ga_run generation; ops per genome = a uniform S_(2,8) genome at k=8 (the "
+                             "random initial population; evolved populations differ)")
+        roof.pop("ops_per_genome_executed"); roof.pop("achieved_executed"); roof.pop("frac_executed")
     return {"metric": "GA generations/sec (JaTAM-shape fitness)", "value": gens / dev_s, "unit": "generations/s",
             "ms_per_generation": dev_s / gens * 1e3, "genomes_classified_per_s": gens * n / dev_s,
             "config": {"workload": "GA toward a 12-cell S_(2,8) target shape, population 2^20, L=24, k=8, d=19, "
                                    "muL=0.3, asexual, random initial population", "generations_timed": gens},
             "best_fitness_seen": best,
             "note": "each generation = k_prepass + key sort + k_classify_fast (fit mode) over 2^20 genomes + one "
-                    "k_ga_run generation; timed with CUDA events on the launch stream"}
+                    "k_ga_run generation; timed with CUDA events on the launch stream",
+            "roofline": roof, "cpu_baseline": cpu}
 
 
 def ga_sweep_bench(runs: int = 100) -> dict:
@@ -504,49 +625,30 @@ def main():
 
     # ---- roofline: dominant kernel vs measured int32 ALU peak
     roof = None
+    peak = int_peak_ops(stream) if rank == 0 else None
     if rank == 0:
-        counts = json.load(open(os.path.join(ROOT, "profiles", "event_counts.json")))["s28_full"]
-        ops_per_genome = counts["ops_per_genome"]
-        nsm = _lib.ctypes.c_int32()
-        L.tv_sm_count(_lib.ctypes.byref(nsm))
-        peak = 0.0
-        for _ in range(3):
-            ops = _lib.ctypes.c_double()
-            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s0.record(stream)
-            _lib.check(L.tv_int_peak_launch(1 << 16, nsm.value * 8, 256, sp, _lib.ctypes.byref(ops)))
-            s1.record(stream)
-            torch.cuda.synchronize()
-            peak = max(peak, ops.value / (s0.elapsed_time(s1) / 1e3))
         kms = statistics.mean(kern_ms) if kern_ms else ms_per_step
-        achieved = ops_per_genome * (N_S28 / world) / (kms / 1e3)
         traffic = None
         try:
             tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))["k_classify_fast<2>"]
             traffic = tr["dram_bytes_read"] + tr["dram_bytes_write"]
         except Exception:
             pass
-        roof = {"bound": "int32_alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tops/s",
-                "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read+write)",
-                "kernel": "k_classify_fast<2>", "kernel_ms": kms,
-                "kernel_ms_covers": "one tv_enumerate_chunks call: k_prepass<2> (trivial-freedom bits + behaviour "
-                                    "key, ~1.3 ms) + CUB radix sort of the keys (~0.2 ms) + k_classify_fast<2> "
-                                    "(conservative: all three kernels' time)",
-                "ops_per_genome": ops_per_genome,
-                "peak_source": "measured on this GPU: tv_int_peak_launch (8 independent IADD3/LOP3 chains/thread)",
-                "ops_source": "event-weighted algorithmic int32 ops (SURVEY.md 8d weights) x oracle event counts, "
-                              "profiles/event_counts.json"}
+        roof = enum_roofline("k_classify_fast<2>", N_S28 / world, kms, peak, event_counts("s28_full"),
+                             "one tv_enumerate_chunks call: k_prepass<2> (trivial-freedom proof, 1-mers, behaviour "
+                             "key, ~1.4 ms) + CUB radix sort of the keys (~0.2 ms) + k_classify_fast<2> "
+                             "(conservative: all three kernels' time)", traffic)
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         try:
             cpu = cpu_port_rate()
         except Exception as e:  # the oracle is test infrastructure; report, do not fail the bench
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {e}"}
-    s32 = None if args.no_s32 else s32_bench(args, rank, world, stream)
+    s32 = None if args.no_s32 else s32_bench(args, rank, world, stream, peak)
     ga = ga_jatam = ga_sweep = None
     if rank == 0 and not args.no_ga:
-        ga = ga_bench(args)
-        ga_jatam = ga_jatam_bench()
+        ga = ga_bench(args, ceil=l2_ceilings(stream))
+        ga_jatam = ga_jatam_bench(peak=peak, cpu_leg=not args.no_cpu_baseline)
         ga_sweep = ga_sweep_bench()
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

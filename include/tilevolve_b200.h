@@ -200,6 +200,13 @@ int tv_ga_fitness_jatam(tv_ga *h, int32_t a, int32_t bpl, const int64_t *mask_po
 /* Launch the int32 ALU peak probe (IADD3/LOP3 chains); *ops = int32 ops issued. */
 int tv_int_peak_launch(int64_t iters, int32_t blocks, int32_t threads, void *stream, double *ops);
 int tv_sm_count(int32_t *n);
+/* L2 ceilings for the GA roofline: read+write streaming over buf (random = 0) or
+ * independent random 16-byte reads (random = 1) of a buffer of `bytes` (size it to stay
+ * L2-resident); *bytes_moved = bytes the launch moves. */
+int tv_l2_probe_launch(void *buf, int64_t bytes, int32_t reps, int32_t random, void *stream, double *bytes_moved);
+/* Grid-barrier floor: one cooperative launch (one 1024-thread CTA per SM, the GA kernel's
+ * geometry) executing `syncs` grid.sync() back to back. */
+int tv_gridsync_probe_launch(int32_t syncs, void *stream);
 
 #ifdef __cplusplus
 }

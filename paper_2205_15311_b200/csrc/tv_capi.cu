@@ -1,4 +1,5 @@
 // tv_capi.cu -- extern "C" boundary of libtilevolve_b200.so (include/tilevolve_b200.h).
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX ranges (no-ops unless a profiler is attached)
 #include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
 
@@ -424,6 +425,20 @@ int fix_payloads(tv_hist *h, cudaStream_t st) {
 }
 }  // namespace
 
+
+// NVTX range around every batch-level C-ABI call (SURVEY section 5 tracing): visible in
+// Nsight Systems / ncu --nvtx timelines, free when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char *name, long long n = -1) {
+    char buf[96];
+    if (n >= 0) snprintf(buf, sizeof buf, "%s n=%lld", name, n);
+    nvtxRangePushA(n >= 0 ? buf : name);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
+
 extern "C" {
 
 int tv_version(void) { return 10000; }
@@ -440,6 +455,7 @@ int tv_classify_batch(const uint64_t *indices, int64_t n, int32_t a, int32_t bpl
                       const int64_t *ks, int64_t q, int32_t hist_k, uint64_t seed, int32_t strict,
                       uint8_t *out_class, uint32_t *out_hash, uint8_t *out_w, uint8_t *out_h, uint16_t *out_cells,
                       uint64_t *out_shape, int64_t W, void *stream) {
+  NvtxRange nvtx_("tv_classify_batch", (long long)n);
   Common C;
   if (n < 0) return fail(TV_ERR_ARG, "negative n");
   if (int rc = fill_common(a, bpl, mask_pos, mask_val, m, free_pos, nfree, d, ks, q, hist_k, seed, strict, C)) return rc;
@@ -667,6 +683,7 @@ int tv_hist_count(tv_hist *h, int64_t *n_keys, int32_t *overflow, void *stream) 
 int tv_hist_export(tv_hist *h, int64_t max_records, uint32_t *keys, uint64_t *det, uint64_t *steric,
                    uint64_t *rep_det, uint64_t *rep_any, uint8_t *w, uint8_t *hh, uint16_t *cells, uint64_t *shape,
                    int64_t *tallies, int64_t *n_out, void *stream) {
+  NvtxRange nvtx_("tv_hist_export");
   if (!h) return fail(TV_ERR_ARG, "null histogram");
   cudaStream_t st = (cudaStream_t)stream;
   int64_t n = 0;
@@ -715,6 +732,7 @@ int tv_hist_export(tv_hist *h, int64_t max_records, uint32_t *keys, uint64_t *de
 
 int tv_hist_pack(tv_hist *h, int64_t max_records, uint64_t *rows, int64_t *tallies, int64_t *n_out,
                  void *stream) {
+  NvtxRange nvtx_("tv_hist_pack");
   if (!h) return fail(TV_ERR_ARG, "null histogram");
   cudaStream_t st = (cudaStream_t)stream;
   int64_t n = 0;
@@ -753,6 +771,7 @@ int tv_hist_pack(tv_hist *h, int64_t max_records, uint64_t *rows, int64_t *talli
 }
 
 int tv_hist_replace_rows(tv_hist *h, int64_t n, const uint64_t *rows, const int64_t *tallies, void *stream) {
+  NvtxRange nvtx_("tv_hist_replace_rows", (long long)n);
   if (!h) return fail(TV_ERR_ARG, "null histogram");
   if (n < 0) return fail(TV_ERR_ARG, "negative n");
   cudaStream_t st = (cudaStream_t)stream;
@@ -838,6 +857,7 @@ static int enumerate_common(const uint64_t *indices, uint64_t start, uint64_t ch
                             const int64_t *mask_pos, const uint8_t *mask_val, int64_t m, const int64_t *free_pos,
                             int64_t nfree, int32_t d, const int64_t *ks, int64_t q, int32_t hist_k, uint64_t seed,
                             int32_t strict, tv_hist *h, void *stream) {
+  NvtxRange nvtx_("tv_enumerate", (long long)count);
   if (!h) return fail(TV_ERR_ARG, "null histogram");
   if (count < 0) return fail(TV_ERR_ARG, "negative count");
   Common C;
@@ -926,6 +946,70 @@ int tv_int_peak_launch(int64_t iters, int32_t blocks, int32_t threads, void *str
   k_int_peak<<<blocks, threads, 0, (cudaStream_t)stream>>>(iters, 12345u, sink);
   CK(cudaGetLastError());
   if (ops) *ops = (double)blocks * threads * (double)iters * 16.0;
+  return 0;
+}
+
+// L2 ceilings for the GA roofline (its working set is L2-resident): streaming read+write of
+// a buffer that fits in L2 (16-byte .cg accesses, grid-stride), or independent random 16-byte
+// reads (the access pattern of roulette selection).
+__global__ void __launch_bounds__(256) k_l2_probe(uint4 *buf, int64_t n16, int32_t reps, int32_t random) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+  if (!random) {
+    for (int r = 0; r < reps; r++)
+      for (int64_t i = tid; i < n16; i += nth) {
+        uint4 v = __ldcg(buf + i);
+        v.x += 1u;
+        __stcg(buf + i, v);
+      }
+  } else {
+    uint32_t acc = 0, x = (uint32_t)tid * 0x9E3779B9u + 12345u;
+    const int64_t per = (n16 + nth - 1) / nth;
+    for (int r = 0; r < reps; r++)
+      for (int64_t k = 0; k < per; k += 4) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {  // 4 independent loads in flight per thread
+          x ^= x << 13; x ^= x >> 17; x ^= x << 5;
+          v[u] = __ldcg(buf + (x % (uint32_t)n16));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) acc += v[u].x ^ v[u].w;
+      }
+    if (acc == 0x12345678u) buf[0].y = acc;  // keep the loads
+  }
+}
+
+// grid-barrier floor: the GA kernel's launch geometry (one 1024-thread CTA per SM), `syncs`
+// grid.sync() calls back to back
+__global__ void __launch_bounds__(1024, 1) k_gridsync_probe(int32_t syncs) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  for (int i = 0; i < syncs; i++) grid.sync();
+}
+
+int tv_l2_probe_launch(void *buf, int64_t bytes, int32_t reps, int32_t random, void *stream, double *bytes_moved) {
+  int dev;
+  if (int rc = current_device(&dev)) return rc;
+  if (!buf || bytes < 16) return fail(TV_ERR_ARG, "probe buffer");
+  int nsm = 0;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t n16 = bytes / 16;
+  k_l2_probe<<<nsm * 8, 256, 0, (cudaStream_t)stream>>>((uint4 *)buf, n16, reps, random);
+  CK(cudaGetLastError());
+  if (bytes_moved) {
+    const int64_t nth = (int64_t)nsm * 8 * 256, per = (n16 + nth - 1) / nth;
+    *bytes_moved = random ? (double)nth * (double)((per + 3) / 4 * 4) * 16.0 * reps : 32.0 * (double)n16 * reps;
+  }
+  return 0;
+}
+
+int tv_gridsync_probe_launch(int32_t syncs, void *stream) {
+  int dev;
+  if (int rc = current_device(&dev)) return rc;
+  int nsm = 0;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  void *args[] = {&syncs};
+  CK(cudaLaunchCooperativeKernel((const void *)k_gridsync_probe, dim3(nsm), dim3(1024), args, 0, (cudaStream_t)stream));
   return 0;
 }
 
@@ -1021,6 +1105,7 @@ int tv_ga_population_ptr(tv_ga *h, uint64_t **dev_ptr) {
 int tv_ga_run(tv_ga *h, uint64_t seed, int64_t g0, int64_t n_gens, uint32_t target, int64_t adapt_count,
               int32_t stop_when, const uint32_t *f_ext, uint32_t *best, uint64_t *sum, uint32_t *count,
               int64_t *gens_done, void *stream) {
+  NvtxRange nvtx_("tv_ga_run", (long long)n_gens);
   if (!h) return fail(TV_ERR_ARG, "null GA");
   if (n_gens < 1) return fail(TV_ERR_ARG, "n_gens must be >= 1");
   if (f_ext && n_gens != 1) return fail(TV_ERR_ARG, "an external fitness vector covers exactly one generation");
@@ -1070,6 +1155,7 @@ int tv_ga_replicas(int64_t n, int32_t L, int32_t mode, const uint64_t *T, int32_
                    const uint64_t *init, int64_t g0, int64_t n_gens, uint32_t target, int64_t adapt_count,
                    int32_t stop_when, int64_t *done, int64_t *disc, int64_t *adapt, uint32_t *best, uint64_t *sum,
                    uint32_t *count, uint64_t *final_pop, void *stream) {
+  NvtxRange nvtx_("tv_ga_replicas", (long long)R);
   if (n < 2 || n > 8192) return fail(TV_ERR_ARG, "replica population %lld outside [2, 8192]", (long long)n);
   if (L < 1 || L > 64) return fail(TV_ERR_ARG, "genome length %d outside [1, 64]", L);
   if (mode < 0 || mode > 2) return fail(TV_ERR_ARG, "reproduction mode %d not in {0,1,2}", mode);
@@ -1126,6 +1212,7 @@ int tv_ga_replicas(int64_t n, int32_t L, int32_t mode, const uint64_t *T, int32_
 int tv_ga_fitness_jatam(tv_ga *h, int32_t a, int32_t bpl, const int64_t *mask_pos, const uint8_t *mask_val,
                         int64_t m, const int64_t *free_pos, int64_t nfree, int32_t d, int32_t k, uint64_t seed,
                         int32_t strict, const uint8_t *target_occ, uint32_t *f_out, void *stream) {
+  NvtxRange nvtx_("tv_ga_fitness_jatam");
   if (!h) return fail(TV_ERR_ARG, "null GA");
   if (d > 29) return fail(TV_ERR_ARG, "JaTAM fitness supports d <= 29");
   if (nfree != h->P.L) return fail(TV_ERR_ARG, "GA genome length %d != %lld free bits", h->P.L, (long long)nfree);

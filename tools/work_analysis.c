@@ -172,10 +172,10 @@ int main(int argc, char **argv) {
     uint64_t tot_pops = 0, tot_runs = 0, om_g = 0, om_pops = 0, om_runs = 0;
     uint64_t au_pops = 0, au_fu_pops = 0, au_fu_tf_pops = 0, au_tr_pops = 0, au_fu_g = 0, au_fu_tf_g = 0;
     uint64_t unb_g = 0, tf_g = 0, tf2_g = 0, au_fu_tf2_pops = 0, au_fu_tf2_g = 0, viol2 = 0, au_runs = 0, au_fu_runs = 0, au_fu_tf_runs = 0;
-    uint64_t ops_ref = 0, ops_exec = 0, runs_exec = 0, pops_exec = 0, fz_g = 0, fz_pops_saved = 0, fz_runs_saved = 0, fz_viol = 0, fz_det = 0, run0_unb_pops = 0, cls[4] = {0, 0, 0, 0}, cls_pops[4] = {0, 0, 0, 0}, det_tf2_pops = 0, det_tf2_g = 0;
+    uint64_t ex_cls[4] = {0, 0, 0, 0}, ex_runs_cls[4] = {0, 0, 0, 0}, ops_ref = 0, ops_exec = 0, runs_exec = 0, pops_exec = 0, fz_g = 0, fz_pops_saved = 0, fz_runs_saved = 0, fz_viol = 0, fz_det = 0, run0_unb_pops = 0, cls[4] = {0, 0, 0, 0}, cls_pops[4] = {0, 0, 0, 0}, det_tf2_pops = 0, det_tf2_g = 0;
 #pragma omp parallel reduction(+ : tot_pops, tot_runs, om_g, om_pops, om_runs, au_pops, au_fu_pops, au_fu_tf_pops, \
                                au_tr_pops, au_fu_g, au_fu_tf_g, unb_g, tf_g, au_runs, au_fu_runs, au_fu_tf_runs, \
-                               ops_ref, ops_exec, runs_exec, pops_exec, fz_g, fz_pops_saved, fz_runs_saved, fz_viol, fz_det, run0_unb_pops, cls[:4], cls_pops[:4], det_tf2_pops, det_tf2_g, tf2_g, au_fu_tf2_pops, au_fu_tf2_g, viol2)
+                               ex_cls[:4], ex_runs_cls[:4], ops_ref, ops_exec, runs_exec, pops_exec, fz_g, fz_pops_saved, fz_runs_saved, fz_viol, fz_det, run0_unb_pops, cls[:4], cls_pops[:4], det_tf2_pops, det_tf2_g, tf2_g, au_fu_tf2_pops, au_fu_tf2_g, viol2)
     {
         orc_scratch S;
         orc_scratch_alloc(&S, d);
@@ -239,7 +239,7 @@ int main(int argc, char **argv) {
                     uint64_t o = 24 * (RC[r].draws + RC[r].pops + RC[r].placements) + 10 * RC[r].hashed_cells +
                                  16 * RC[r].bounded_runs + 16 * RC[r].runs;
                     ops_ref += o;
-                    if (r < ne) { ops_exec += o; runs_exec++; pops_exec += RC[r].pops; }
+                    if (r < ne) { ops_exec += o; runs_exec++; pops_exec += RC[r].pops; ex_cls[c] += RC[r].pops; ex_runs_cls[c]++; }
                 }
                 ops_ref += 64;
                 ops_exec += om ? 16 : 64;
@@ -297,6 +297,9 @@ int main(int argc, char **argv) {
     printf(" \"ops_per_genome_reference\": %.2f, \"ops_per_genome_executed\": %.2f, \"runs_executed\": %llu, \"pops_executed\": %llu,\n",
            (double)ops_ref / (double)count, (double)ops_exec / (double)count, (unsigned long long)runs_exec,
            (unsigned long long)pops_exec);
+    printf(" \"executed_pops_by_class\": [%llu, %llu, %llu, %llu], \"executed_runs_by_class\": [%llu, %llu, %llu, %llu],\n",
+           (unsigned long long)ex_cls[0], (unsigned long long)ex_cls[1], (unsigned long long)ex_cls[2], (unsigned long long)ex_cls[3],
+           (unsigned long long)ex_runs_cls[0], (unsigned long long)ex_runs_cls[1], (unsigned long long)ex_runs_cls[2], (unsigned long long)ex_runs_cls[3]);
     printf(" \"run0_unbound_later_pops\": %llu}\n", (unsigned long long)run0_unb_pops);
     return 0;
 }
