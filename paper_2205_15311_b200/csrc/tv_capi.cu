@@ -962,18 +962,22 @@ __global__ void __launch_bounds__(256) k_l2_probe(uint4 *buf, int64_t n16, int32
         __stcg(buf + i, v);
       }
   } else {
-    uint32_t acc = 0, x = (uint32_t)tid * 0x9E3779B9u + 12345u;
+    // n16 rounded down to a power of two: the index is a mask of a Weyl sequence through a
+    // multiplicative hash (a few integer ops per load, so the probe is bound by L2, not issue)
+    uint32_t m = 1u;
+    while ((int64_t)m * 2 <= n16) m *= 2;
+    uint32_t acc = 0, x = (uint32_t)tid * 0x9E3779B9u;
     const int64_t per = (n16 + nth - 1) / nth;
     for (int r = 0; r < reps; r++)
-      for (int64_t k = 0; k < per; k += 4) {
-        uint4 v[4];
+      for (int64_t k = 0; k < per; k += 8) {
+        uint4 v[8];
 #pragma unroll
-        for (int u = 0; u < 4; u++) {  // 4 independent loads in flight per thread
-          x ^= x << 13; x ^= x >> 17; x ^= x << 5;
-          v[u] = __ldcg(buf + (x % (uint32_t)n16));
+        for (int u = 0; u < 8; u++) {  // 8 independent loads in flight per thread
+          x += 0x6D2B79F5u;
+          v[u] = __ldcg(buf + (((x ^ (x >> 15)) * 0x2C1B3C6Du >> 7) & (m - 1u)));
         }
 #pragma unroll
-        for (int u = 0; u < 4; u++) acc += v[u].x ^ v[u].w;
+        for (int u = 0; u < 8; u++) acc += v[u].x ^ v[u].w;
       }
     if (acc == 0x12345678u) buf[0].y = acc;  // keep the loads
   }
@@ -998,7 +1002,7 @@ int tv_l2_probe_launch(void *buf, int64_t bytes, int32_t reps, int32_t random, v
   CK(cudaGetLastError());
   if (bytes_moved) {
     const int64_t nth = (int64_t)nsm * 8 * 256, per = (n16 + nth - 1) / nth;
-    *bytes_moved = random ? (double)nth * (double)((per + 3) / 4 * 4) * 16.0 * reps : 32.0 * (double)n16 * reps;
+    *bytes_moved = random ? (double)nth * (double)((per + 7) / 8 * 8) * 16.0 * reps : 32.0 * (double)n16 * reps;
   }
   return 0;
 }
@@ -1045,7 +1049,7 @@ int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **
   for (int j = 0; j < 64; j++) P.T[j] = j < L ? T[j] : ~0ULL;
   h->smem = 0;
   int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ga_run, 1024, h->smem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ga_run, TV_GA_THREADS, h->smem));
   if (per_sm < 1) { delete h; return fail(TV_ERR_CUDA, "GA kernel does not fit one CTA per SM"); }
   h->nblocks = nsm;
   if (const char *ec = getenv("TV_GA_CTAS")) h->nblocks = std::max(1, std::min(nsm, atoi(ec)));  // A/B only
@@ -1129,8 +1133,8 @@ int tv_ga_run(tv_ga *h, uint64_t seed, int64_t g0, int64_t n_gens, uint32_t targ
     const bool prof = getenv("TV_GA_PROF") != nullptr;  // phase timing of CTA 0 (development aid)
     if (prof) { CK(S.get(&P.prof, 3)); CK(cudaMemsetAsync(P.prof, 0, 24, st)); }
     void *args[] = {&P};
-    CK(cudaLaunchCooperativeKernel((const void *)k_ga_run, dim3(h->nblocks), dim3(1024), args, h->smem, st));
-    g_launch[0] = 3; g_launch[1] = h->nblocks; g_launch[2] = 1024; g_launch[3] = (int64_t)h->smem; g_launch[4] = 1;
+    CK(cudaLaunchCooperativeKernel((const void *)k_ga_run, dim3(h->nblocks), dim3(TV_GA_THREADS), args, h->smem, st));
+    g_launch[0] = 3; g_launch[1] = h->nblocks; g_launch[2] = TV_GA_THREADS; g_launch[3] = (int64_t)h->smem; g_launch[4] = 1;
     CK(cudaMemcpyAsync(&done, P.done, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&fb, P.final_buf, 4, cudaMemcpyDeviceToHost, st));
     if (best) CK(cudaMemcpyAsync(best, d_best, n_gens * 4, cudaMemcpyDefault, st));

@@ -32,6 +32,9 @@
 
 #include "tv_device.cuh"
 
+#ifndef TV_GA_THREADS
+#define TV_GA_THREADS 1024  // k_ga_run CTA size (one CTA per SM)
+#endif
 #ifndef TV_GA_ILP
 #define TV_GA_ILP 1  // children per thread in flight in phase C (2 and 3 measured 0.7-2 % slower, 4 and 8 more)
 #endif
@@ -198,10 +201,10 @@ __device__ __forceinline__ uint32_t ga_rows_scan(uint32_t *rowx, int nrows, uint
 //      consecutive children at a time, so the row's fitness sum, best and count for the
 //      next generation come from warp reductions, and a block scan of the row sums
 //      replaces a separate pass over the staged fitness.
-__global__ void __launch_bounds__(1024, 1) k_ga_run(const __grid_constant__ GaParams P) {
+__global__ void __launch_bounds__(TV_GA_THREADS, 1) k_ga_run(const __grid_constant__ GaParams P) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
-  __shared__ uint32_t warp_sum[33];  // blockDim.x == 1024
+  __shared__ uint32_t warp_sum[33];  // blockDim.x <= 1024
   __shared__ uint32_t s_best, s_cnt, s_carry;
   __shared__ unsigned long long s_off, s_total;
   __shared__ int s_stop;
