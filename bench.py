@@ -321,7 +321,17 @@ def ga_bench(args, n: int = 1 << 20, gens: int = 2000, ceil: dict | None = None)
                                                          "tv_gridsync_probe_launch on this GPU",
                              "frac_l2_stream": 16.0 * n * k / dev_s / 1e9 / ceil["l2_stream_gbs"],
                              "barrier_floor_us_per_generation": 2 * ceil["grid_sync_us"],
-                             "frac_of_barrier_floor": 2 * ceil["grid_sync_us"] / (dev_s / k * 1e6)}},
+                             "frac_of_barrier_floor": 2 * ceil["grid_sync_us"] / (dev_s / k * 1e6),
+                             # composite floor of this kernel's own traffic: two grid barriers + one random
+                             # 16-byte guide read per child at the random-L2 rate + the streamed bytes
+                             # (phase B: fitness 4 + packed word 8 read, word 8 + guide 16 written; phase C:
+                             # child 8 + fitness 4 written) at the streaming-L2 rate
+                             "composite_floor_us_per_generation": (
+                                 2 * ceil["grid_sync_us"] + 16.0 * n / (ceil["l2_random16_gbs"] * 1e3)
+                                 + 48.0 * n / (ceil["l2_stream_gbs"] * 1e3)),
+                             "frac_of_composite_floor": (
+                                 2 * ceil["grid_sync_us"] + 16.0 * n / (ceil["l2_random16_gbs"] * 1e3)
+                                 + 48.0 * n / (ceil["l2_stream_gbs"] * 1e3)) / (dev_s / k * 1e6)}},
             "cpu_baseline": {"value": cg / cpu_s, "unit": "generations/s", "cores": os.cpu_count(),
                              "kind": "restatement (no reference GA exists)",
                              "sample": f"{cg} generations of 2^20 on oracle/tv_ga_oracle.c, OpenMP"}}
@@ -480,6 +490,37 @@ def ga_jatam_bench(n: int = 1 << 20, gens: int = 20, peak: float | None = None, 
             "note": "each generation = k_prepass + key sort + k_classify_fast (fit mode) over 2^20 genomes + one "
                     "k_ga_run generation; timed with CUDA events on the launch stream",
             "roofline": roof, "cpu_baseline": cpu}
+
+
+def mutation_bench(cpu_leg: bool = True) -> dict:
+    """SPEC ACCEPTANCE 8 (Fig. 5's regime): mutating 2^20 genomes of L = 1024 bits at muL = 0.5 by
+    distribution (the GA operator) vs bit-by-bit flipping, device-timed; the same pair of
+    operators on the host cores (oracle/tv_ga_oracle.c orc_ga_mutate) beside it."""
+    from paper_2205_15311_b200 import evolve as E
+    r = E.mutation_benchmark(pop_size=1 << 20, length=1024, mu_L=0.5, reps=5)
+    out = {"metric": "mutation speed-up, distribution vs bit-by-bit (L=1024, muL=0.5)", "value": r["speedup"],
+           "unit": "x", "higher_is_better": True,
+           "config": {"workload": "mutate 2^20 genomes x 1024 bits, muL = 0.5, one generation per timed call",
+                      "pop_size": r["pop_size"], "L": 1024, "muL": 0.5},
+           "distribution_ms": r["distribution_ms"], "bitwise_ms": r["bitwise_ms"],
+           "distribution_genomes_per_s": (1 << 20) / (r["distribution_ms"] / 1e3),
+           "flips_per_genome": [r["distribution_flips_per_genome"], r["bitwise_flips_per_genome"]],
+           "spec": "SPEC ACCEPTANCE 8: >= 2x"}
+    if cpu_leg:
+        from oracle import oracle as O
+        n = 1 << 16
+        T = E.poisson_thresholds(0.5, 1024)
+        ts = []
+        for method in (0, 1):
+            pop = np.zeros((n, 16), np.uint64)
+            O.ga_mutate(pop[:1024], 1024, T, E.bernoulli_threshold(0.5, 1024), method, 0, 0)
+            t = time.perf_counter()
+            O.ga_mutate(pop, 1024, T, E.bernoulli_threshold(0.5, 1024), method, 0, 1)
+            ts.append(time.perf_counter() - t)
+        out["cpu_baseline"] = {"value": ts[1] / ts[0], "unit": "x", "cores": os.cpu_count(), "kind": "restatement",
+                               "sample": f"{n} genomes x 1024 bits, both operators on oracle/tv_ga_oracle.c, OpenMP "
+                                         f"({ts[0] * 1e3:.2f} ms vs {ts[1] * 1e3:.1f} ms)"}
+    return out
 
 
 def ga_sweep_bench(runs: int = 100) -> dict:
@@ -645,11 +686,12 @@ def main():
         except Exception as e:  # the oracle is test infrastructure; report, do not fail the bench
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {e}"}
     s32 = None if args.no_s32 else s32_bench(args, rank, world, stream, peak)
-    ga = ga_jatam = ga_sweep = None
+    ga = ga_jatam = ga_sweep = mutation = None
     if rank == 0 and not args.no_ga:
         ga = ga_bench(args, ceil=l2_ceilings(stream))
         ga_jatam = ga_jatam_bench(peak=peak, cpu_leg=not args.no_cpu_baseline)
         ga_sweep = ga_sweep_bench()
+        mutation = mutation_bench(cpu_leg=not args.no_cpu_baseline)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
@@ -665,7 +707,7 @@ def main():
                 # ours per step: k_hist_reset, k_prepass, k_classify_fast (+ at N > 1 the exchange:
                 # k_hist_compact, k_hist_pack, k_hist_reset, k_hist_merge, k_hist_merge_rows1/2)
                 "gpu_launches": (3 if world == 1 else 9) * args.steps, "s32": s32, "ga": ga, "ga_jatam": ga_jatam,
-                "ga_sweep": ga_sweep}
+                "ga_sweep": ga_sweep, "mutation_L1024": mutation}
         print(json.dumps(line), flush=True)
     hist.close()
     if world > 1:

@@ -162,10 +162,13 @@ int tv_enumerate_indices(const uint64_t *indices, int64_t n, int32_t a, int32_t 
 
 /* ---- GA generation loop (semantics in oracle/tv_ga_oracle.c) */
 typedef struct tv_ga tv_ga;
-/* n genomes of L <= 64 bits (integer = genome.to_int()); mode 0 asexual,
- * 1 single-point crossover, 2 uniform crossover; T[L] = Poisson(lambda) CDF
- * thresholds x 2^63 (k flips = #{j : (draw >> 1) >= T[j]}).  Population
- * starts all-zero. */
+/* n genomes of L <= 4096 bits; mode 0 asexual, 1 single-point crossover, 2 uniform
+ * crossover; T[L] = Poisson(lambda) CDF thresholds x 2^63 (k flips = #{j : (draw >> 1)
+ * >= T[j]}).  Population starts all-zero.  L <= 64: one u64 per genome (the integer
+ * genome.to_int()), one cooperative kernel per tv_ga_run.  L > 64: W = ceil(L/64)
+ * little-endian u64 words per genome (set/get_population take [n, W] genome-major
+ * arrays; the device keeps them word-major), three launches per generation
+ * (orc_ga_run_w semantics); external / JaTAM fitness and tv_ga_replicas need L <= 64. */
 int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **out);
 int tv_ga_destroy(tv_ga *h);
 int tv_ga_set_population(tv_ga *h, const uint64_t *genomes, void *stream);  /* [h|d]; NULL = zeros */
@@ -195,6 +198,14 @@ int tv_ga_replicas(int64_t n, int32_t L, int32_t mode, const uint64_t *T, int32_
 int tv_ga_fitness_jatam(tv_ga *h, int32_t a, int32_t bpl, const int64_t *mask_pos, const uint8_t *mask_val,
                         int64_t m, const int64_t *free_pos, int64_t nfree, int32_t d, int32_t k, uint64_t seed,
                         int32_t strict, const uint8_t *target_occ, uint32_t *f_out, void *stream);
+
+/* SPEC ACCEPTANCE 8 mutation benchmark (orc_ga_mutate semantics): mutate the word-major
+ * device population pop [W x n] of L-bit genomes in place with stream (seed, g, i);
+ * method 0 = by distribution (the GA's operator, T host or device), 1 = bit by bit (one
+ * draw per bit, flip when draw < pthr).  flips (host, may be NULL) = total flips;
+ * synchronises only when flips is given. */
+int tv_ga_mutate(uint64_t *pop, int64_t n, int32_t L, const uint64_t *T, uint64_t pthr, int32_t method,
+                 uint64_t seed, int64_t g, uint64_t *flips, void *stream);
 
 /* ---- measurement helpers (bench.py roofline) */
 /* Launch the int32 ALU peak probe (IADD3/LOP3 chains); *ops = int32 ops issued. */

@@ -52,6 +52,13 @@ def lib():
         L.orc_ga_child.argtypes = [_u64, _i64, _i64, _p, _p, _i64, _i32, _i32, _p]
         L.orc_ga_draws.restype = None
         L.orc_ga_draws.argtypes = [_u64, _u64, _u64, _i64, _p]
+        L.orc_ga_run_w.restype = _i64
+        L.orc_ga_run_w.argtypes = [_p, _i64, _i32, _i32, _p, _u64, _i64, _i64, ctypes.c_uint32, _i64, _i32,
+                                   _p, _p, _p, _i32]
+        L.orc_ga_child_w.restype = None
+        L.orc_ga_child_w.argtypes = [_u64, _i64, _i64, _p, _p, _i64, _i32, _i32, _p, _p]
+        L.orc_ga_mutate.restype = _u64
+        L.orc_ga_mutate.argtypes = [_p, _i64, _i32, _p, _u64, _i32, _u64, _i64, _i32]
         L.orc_ga_flip_counts.restype = None
         L.orc_ga_flip_counts.argtypes = [_u64, _i64, _i32, _p, _p]
         L.orc_stream_draws.restype = None
@@ -150,3 +157,34 @@ def ga_flip_counts(seed, n, L, T) -> np.ndarray:
     T = np.ascontiguousarray(T, np.uint64)
     lib().orc_ga_flip_counts(int(seed), n, L, _ptr(T), _ptr(out))
     return out
+
+
+def ga_run_w(pop: np.ndarray, L: int, mode: int, T: np.ndarray, seed: int, g0: int, n_gens: int, target: int,
+             adapt_count: int, stop_when: int, nthreads: int = 0):
+    """Wide genomes: pop u64 [n, W] (little-endian words), in place; as ga_run otherwise."""
+    assert pop.dtype == np.uint64 and pop.flags.c_contiguous and pop.ndim == 2
+    T = np.ascontiguousarray(T, np.uint64)
+    best = np.zeros(n_gens, np.uint32)
+    sm = np.zeros(n_gens, np.uint64)
+    cnt = np.zeros(n_gens, np.uint32)
+    done = lib().orc_ga_run_w(_ptr(pop), pop.shape[0], L, mode, _ptr(T), int(seed), g0, n_gens, target,
+                              adapt_count, stop_when, _ptr(best), _ptr(sm), _ptr(cnt), nthreads)
+    return int(done), best[:done], sm[:done], cnt[:done]
+
+
+def ga_child_w(seed, g, i, pop, cdf, L, mode, T) -> np.ndarray:
+    pop = np.ascontiguousarray(pop, np.uint64)
+    cdf = np.ascontiguousarray(cdf, np.uint64)
+    T = np.ascontiguousarray(T, np.uint64)
+    out = np.zeros(pop.shape[1], np.uint64)
+    lib().orc_ga_child_w(int(seed), g, i, _ptr(pop), _ptr(cdf), pop.shape[0], L, mode, _ptr(T), _ptr(out))
+    return out
+
+
+def ga_mutate(pop: np.ndarray, L: int, T: np.ndarray, pthr: int, method: int, seed: int, g: int,
+              nthreads: int = 0) -> int:
+    """SPEC ACCEPTANCE 8 operator benchmark (in place): method 0 by distribution, 1 bit by bit."""
+    assert pop.dtype == np.uint64 and pop.flags.c_contiguous and pop.ndim == 2
+    T = np.ascontiguousarray(T, np.uint64)
+    return int(lib().orc_ga_mutate(_ptr(pop), pop.shape[0], L, _ptr(T), int(pthr), method, int(seed), g,
+                                   nthreads))

@@ -160,3 +160,156 @@ void orc_ga_draws(uint64_t seed, uint64_t g, uint64_t i, int64_t n, uint64_t *ou
     uint64_t s = ga_stream(seed, g, i);
     for (int64_t j = 0; j < n; j++) out[j] = ga_draw(&s);
 }
+
+/*
+ * Wide genomes (any L >= 1; used for L > 64): W = ceil(L/64) u64 words per genome,
+ * little-endian (word 0 = integer bits 0..63 of genome.to_int()), genome position p is
+ * integer bit L-1-p, population stored genome-major (pop[i*W + w]).  Draw order per child
+ * is the narrow one with the uniform-crossover mask drawn one word at a time (word 0
+ * first): a, [b], [p = below(L) | W mask draws], u, flip positions.  For W = 1 every
+ * operator is identical to orc_ga_child (checked in tests/test_ga.py).  Fitness = total
+ * popcount; the CDF is 64-bit (N x L may exceed 2^32).
+ */
+static int64_t ga_select64(uint64_t *s, const uint64_t *cdf, int64_t n) {
+    const uint64_t total = cdf[n - 1];
+    const uint64_t x = ga_draw(s);
+    if (total == 0) return (int64_t)ga_mulhi(x, (uint64_t)n);
+    const uint64_t r = ga_mulhi(x, total);
+    int64_t lo = 0, hi = n - 1;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (cdf[mid] > r) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+
+static inline uint64_t ga_wfull(int L, int w) {  /* valid integer bits of word w */
+    const int hi = L - 64 * w;
+    return hi >= 64 ? ~0ULL : ((1ULL << hi) - 1);
+}
+
+void orc_ga_child_w(uint64_t seed, int64_t g, int64_t i, const uint64_t *pop, const uint64_t *cdf, int64_t n,
+                    int L, int mode, const uint64_t *T, uint64_t *out) {
+    const int W = (L + 63) / 64;
+    uint64_t s = ga_stream(seed, (uint64_t)g, (uint64_t)i);
+    const uint64_t *a = pop + (size_t)ga_select64(&s, cdf, n) * W;
+    for (int w = 0; w < W; w++) out[w] = a[w];
+    if (mode != 0) {
+        const uint64_t *b = pop + (size_t)ga_select64(&s, cdf, n) * W;
+        if (mode == 1) {  /* positions < p (integer bits >= L-p) from a, the rest from b */
+            const uint32_t p = ga_below(&s, (uint32_t)L);
+            const int lo = L - (int)p;
+            for (int w = 0; w < W; w++) {
+                uint64_t top;
+                if (lo <= 64 * w) top = ~0ULL;
+                else if (lo >= 64 * w + 64) top = 0;
+                else top = ~((1ULL << (lo - 64 * w)) - 1);
+                top &= ga_wfull(L, w);
+                out[w] = (a[w] & top) | (b[w] & ~top & ga_wfull(L, w));
+            }
+        } else {
+            for (int w = 0; w < W; w++) {
+                const uint64_t m = ga_draw(&s) & ga_wfull(L, w);
+                out[w] = (a[w] & ~m) | (b[w] & m);
+            }
+        }
+    }
+    const uint64_t u = ga_draw(&s) >> 1;
+    int k = 0;
+    while (k < L && u >= T[k]) k++;
+    uint64_t *chosen = (uint64_t *)calloc((size_t)W, 8);
+    for (int f = 0; f < k;) {
+        const uint32_t p = ga_below(&s, (uint32_t)L);
+        const int bit = L - 1 - (int)p;
+        if ((chosen[bit >> 6] >> (bit & 63)) & 1) continue;
+        chosen[bit >> 6] |= 1ULL << (bit & 63);
+        f++;
+    }
+    for (int w = 0; w < W; w++) out[w] = (out[w] ^ chosen[w]) & ga_wfull(L, w);
+    free(chosen);
+}
+
+int64_t orc_ga_run_w(uint64_t *pop, int64_t n, int L, int mode, const uint64_t *T, uint64_t seed, int64_t g0,
+                     int64_t n_gens, uint32_t target, int64_t adapt_count, int stop_when,
+                     uint32_t *best, uint64_t *sum, uint32_t *count, int nthreads) {
+#ifdef _OPENMP
+    if (nthreads <= 0) nthreads = omp_get_max_threads();
+#else
+    nthreads = 1;
+#endif
+    const int W = (L + 63) / 64;
+    uint64_t *cdf = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)n);
+    uint64_t *next = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)n * W);
+    int64_t done = 0;
+    for (int64_t t = 0; t < n_gens; t++) {
+        const int64_t g = g0 + t;
+        uint64_t acc = 0, cnt = 0;
+        uint32_t bst = 0;
+        for (int64_t i = 0; i < n; i++) {
+            uint32_t f = 0;
+            for (int w = 0; w < W; w++) f += (uint32_t)__builtin_popcountll(pop[i * W + w]);
+            acc += f;
+            cdf[i] = acc;
+            if (f > bst) bst = f;
+            cnt += f >= target;
+        }
+        if (best) best[t] = bst;
+        if (sum) sum[t] = acc;
+        if (count) count[t] = (uint32_t)cnt;
+        done = t + 1;
+        if ((stop_when == 1 && cnt >= 1) || (stop_when == 2 && (int64_t)cnt >= adapt_count)) break;
+#pragma omp parallel for num_threads(nthreads) schedule(static)
+        for (int64_t i = 0; i < n; i++) orc_ga_child_w(seed, g, i, pop, cdf, n, L, mode, T, next + i * W);
+        memcpy(pop, next, sizeof(uint64_t) * (size_t)n * W);
+    }
+    free(cdf);
+    free(next);
+    return done;
+}
+
+/*
+ * SPEC ACCEPTANCE 8 (mutation benchmark, Fig. 5's regime): mutate n genomes of L bits in
+ * place, `method` 0 = by distribution (k ~ Poisson(lambda) from T, then k distinct
+ * positions: the GA's operator), 1 = bit by bit (one draw per bit, flip when the draw is
+ * below p = lambda / L as a 64-bit threshold `pthr`).  Child i of generation g uses stream
+ * (seed, g, i).  Returns the number of flips (a checksum the caller can compare).
+ */
+uint64_t orc_ga_mutate(uint64_t *pop, int64_t n, int L, const uint64_t *T, uint64_t pthr, int method, uint64_t seed,
+                       int64_t g, int nthreads) {
+#ifdef _OPENMP
+    if (nthreads <= 0) nthreads = omp_get_max_threads();
+#else
+    nthreads = 1;
+#endif
+    const int W = (L + 63) / 64;
+    uint64_t flips = 0;
+#pragma omp parallel for num_threads(nthreads) schedule(static) reduction(+ : flips)
+    for (int64_t i = 0; i < n; i++) {
+        uint64_t s = ga_stream(seed, (uint64_t)g, (uint64_t)i);
+        uint64_t *x = pop + i * W;
+        if (method == 0) {
+            const uint64_t u = ga_draw(&s) >> 1;
+            int k = 0;
+            while (k < L && u >= T[k]) k++;
+            uint64_t chosen[64] = {0};  /* L <= 4096 */
+            for (int f = 0; f < k;) {
+                const uint32_t p = ga_below(&s, (uint32_t)L);
+                const int bit = L - 1 - (int)p;
+                if ((chosen[bit >> 6] >> (bit & 63)) & 1) continue;
+                chosen[bit >> 6] |= 1ULL << (bit & 63);
+                f++;
+            }
+            for (int w = 0; w < W; w++) x[w] ^= chosen[w];
+            flips += (uint64_t)k;
+        } else {
+            for (int p = 0; p < L; p++) {
+                if (ga_draw(&s) < pthr) {
+                    const int bit = L - 1 - p;
+                    x[bit >> 6] ^= 1ULL << (bit & 63);
+                    flips++;
+                }
+            }
+        }
+    }
+    return flips;
+}

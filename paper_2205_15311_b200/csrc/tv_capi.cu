@@ -1,6 +1,7 @@
 // tv_capi.cu -- extern "C" boundary of libtilevolve_b200.so (include/tilevolve_b200.h).
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX ranges (no-ops unless a profiler is attached)
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -181,8 +182,9 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
     // tunables (env overrides exist for A/B measurements only)
     const char *es = getenv("TV_STACK_S"), *ec = getenv("TV_CTA_SLOTS"), *et = getenv("TV_SERVICE_THRESH");
     const char *eth = getenv("TV_FAST_THREADS");
-    // parked lanes that trigger a service pass (measured: a = 2 best at 12, a = 3 at 20)
-    P.service_thresh = et ? atoi(et) : (P.a == 3 ? 20 : 12);
+    // parked lanes that trigger a service pass (measured: a = 2 best at 14 after the round-2 work
+    // elimination, 18.62 vs 18.82 ms at 12; a = 3 at 16-20)
+    P.service_thresh = et ? atoi(et) : (P.a == 3 ? 20 : 14);
     // locally-forced run-0 assemblies end the genome DET after one run (TV_FORCED=0 disables)
     const char *efz = getenv("TV_FORCED");
     P.forced_check = efz ? (atoi(efz) != 0) : 1;
@@ -1031,19 +1033,53 @@ struct tv_ga {
   int cur;  // which population buffer is current
   int nblocks;
   size_t smem;
+  // wide genomes (L > 64): word-major populations in P.pop0 / P.pop1 (W x n words)
+  int W;                            // words per genome (1 = the narrow cooperative kernel)
+  uint64_t *Tw;                     // L thresholds (device)
+  unsigned long long *fw, *cdfw;    // n fitness / inclusive CDF (64-bit)
+  int32_t *flags;                   // [stopped, final parity]
+  unsigned long long *donew;
+  void *scan_tmp;
+  size_t scan_bytes;
 };
 
 int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **out) {
   if (n < 2 || n > ((int64_t)1 << 28)) return fail(TV_ERR_ARG, "population %lld outside [2, 2^28]", (long long)n);
-  if (L < 1 || L > 64) return fail(TV_ERR_ARG, "genome length %d outside [1, 64]", L);
+  if (L < 1 || L > 64 * kGaMaxWords) return fail(TV_ERR_ARG, "genome length %d outside [1, %d]", L, 64 * kGaMaxWords);
   if (mode < 0 || mode > 2) return fail(TV_ERR_ARG, "reproduction mode %d not in {0,1,2}", mode);
-  if ((uint64_t)L * (uint64_t)n >= ((uint64_t)1 << 32)) return fail(TV_ERR_ARG, "L * population must be < 2^32");
+  if (L <= 64 && (uint64_t)L * (uint64_t)n >= ((uint64_t)1 << 32)) return fail(TV_ERR_ARG, "L * population must be < 2^32");
   int dev;
   if (int rc = current_device(&dev)) return rc;
   int nsm = 0;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  if (L > 64) {  // wide genomes: per-generation launches over word-major populations
+    tv_ga *h = new tv_ga();
+    memset(&h->P, 0, sizeof h->P);
+    h->P.n = n; h->P.L = L; h->P.mode = mode;
+    h->W = (L + 63) / 64;
+    h->device = dev;
+    h->cur = 0;
+    cudaError_t e = cudaSuccess;
+    const size_t words = (size_t)n * h->W;
+    e = e ? e : cudaMalloc(&h->P.pop0, words * 8);
+    e = e ? e : cudaMalloc(&h->P.pop1, words * 8);
+    e = e ? e : cudaMalloc(&h->Tw, (size_t)L * 8);
+    e = e ? e : cudaMalloc(&h->fw, (size_t)n * 8);
+    e = e ? e : cudaMalloc(&h->cdfw, (size_t)n * 8);
+    e = e ? e : cudaMalloc(&h->flags, 8);
+    e = e ? e : cudaMalloc(&h->donew, 8);
+    e = e ? e : cudaMemset(h->P.pop0, 0, words * 8);
+    e = e ? e : cudaMemcpy(h->Tw, T, (size_t)L * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+      e = cub::DeviceScan::InclusiveSum(nullptr, h->scan_bytes, h->fw, h->cdfw, (int)n);
+    e = e ? e : cudaMalloc(&h->scan_tmp, std::max<size_t>(h->scan_bytes, 16));
+    if (e != cudaSuccess) { tv_ga_destroy(h); return fail(TV_ERR_CUDA, "GA allocation: %s", cudaGetErrorString(e)); }
+    *out = h;
+    return 0;
+  }
   tv_ga *h = new tv_ga();
   memset(&h->P, 0, sizeof h->P);
+  h->W = 1;
   GaParams &P = h->P;
   P.n = n; P.L = L; P.mode = mode;
   for (int j = 0; j < 64; j++) P.T[j] = j < L ? T[j] : ~0ULL;
@@ -1078,6 +1114,7 @@ int tv_ga_destroy(tv_ga *h) {
   cudaFree(P.pop0); cudaFree(P.pop1); cudaFree(P.cdf); cudaFree(P.guide); cudaFree(P.fstage); cudaFree(P.tot);
   cudaFree(P.rowx);
   cudaFree(P.done); cudaFree(P.final_buf);
+  cudaFree(h->Tw); cudaFree(h->fw); cudaFree(h->cdfw); cudaFree(h->flags); cudaFree(h->donew); cudaFree(h->scan_tmp);
   delete h;
   return 0;
 }
@@ -1086,8 +1123,20 @@ int tv_ga_set_population(tv_ga *h, const uint64_t *genomes, void *stream) {
   if (!h) return fail(TV_ERR_ARG, "null GA");
   cudaStream_t st = (cudaStream_t)stream;
   unsigned long long *dst = h->cur ? h->P.pop1 : h->P.pop0;
-  if (!genomes) CK(cudaMemsetAsync(dst, 0, h->P.n * 8, st));
-  else CK(cudaMemcpyAsync(dst, genomes, h->P.n * 8, cudaMemcpyDefault, st));
+  const int64_t words = h->P.n * h->W;
+  if (!genomes) {
+    CK(cudaMemsetAsync(dst, 0, words * 8, st));
+  } else if (h->W == 1) {
+    CK(cudaMemcpyAsync(dst, genomes, h->P.n * 8, cudaMemcpyDefault, st));
+  } else {  // host / caller layout [n, W] -> device word-major [W, n]
+    Scratch S(st);
+    unsigned long long *tmp;
+    CK(S.get(&tmp, (size_t)words));
+    CK(cudaMemcpyAsync(tmp, genomes, words * 8, cudaMemcpyDefault, st));
+    k_gaw_transpose<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(tmp, dst, h->P.n, h->W, 1);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+  }
   CK(cudaStreamSynchronize(st));
   return 0;
 }
@@ -1095,7 +1144,19 @@ int tv_ga_set_population(tv_ga *h, const uint64_t *genomes, void *stream) {
 int tv_ga_get_population(tv_ga *h, uint64_t *out, void *stream) {
   if (!h) return fail(TV_ERR_ARG, "null GA");
   cudaStream_t st = (cudaStream_t)stream;
-  CK(cudaMemcpyAsync(out, h->cur ? h->P.pop1 : h->P.pop0, h->P.n * 8, cudaMemcpyDefault, st));
+  const unsigned long long *src = h->cur ? h->P.pop1 : h->P.pop0;
+  if (h->W == 1) {
+    CK(cudaMemcpyAsync(out, src, h->P.n * 8, cudaMemcpyDefault, st));
+  } else {  // device word-major [W, n] -> caller layout [n, W]
+    const int64_t words = h->P.n * h->W;
+    Scratch S(st);
+    unsigned long long *tmp;
+    CK(S.get(&tmp, (size_t)words));
+    k_gaw_transpose<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(src, tmp, h->P.n, h->W, 0);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, tmp, words * 8, cudaMemcpyDefault, st));
+    CK(cudaStreamSynchronize(st));
+  }
   CK(cudaStreamSynchronize(st));
   return 0;
 }
@@ -1115,6 +1176,50 @@ int tv_ga_run(tv_ga *h, uint64_t seed, int64_t g0, int64_t n_gens, uint32_t targ
   if (f_ext && n_gens != 1) return fail(TV_ERR_ARG, "an external fitness vector covers exactly one generation");
   if (f_ext && !is_device_ptr(f_ext)) return fail(TV_ERR_ARG, "external fitness must be a device pointer");
   cudaStream_t st = (cudaStream_t)stream;
+  if (h->W > 1) {
+    if (f_ext) return fail(TV_ERR_ARG, "external fitness needs L <= 64");
+    GaWideParams Q;
+    memset(&Q, 0, sizeof Q);
+    Q.n = h->P.n; Q.L = h->P.L; Q.W = h->W; Q.mode = h->P.mode; Q.target = target; Q.adapt_count = adapt_count;
+    Q.stop_when = stop_when; Q.seed = seed; Q.T = h->Tw; Q.f = h->fw; Q.cdf = h->cdfw;
+    Q.stopped = h->flags; Q.final_par = h->flags + 1; Q.done = h->donew;
+    Scratch S(st);
+    uint32_t *d_best, *d_count; unsigned long long *d_sum;
+    CK(S.get(&d_best, n_gens)); CK(S.get(&d_count, n_gens)); CK(S.get(&d_sum, n_gens));
+    CK(cudaMemsetAsync(d_best, 0, n_gens * 4, st));
+    CK(cudaMemsetAsync(d_count, 0, n_gens * 4, st));
+    CK(cudaMemsetAsync(d_sum, 0, n_gens * 8, st));
+    const int32_t init_flags[2] = {0, -1};
+    CK(cudaMemcpyAsync(h->flags, init_flags, 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(h->donew, 0, 8, st));
+    Q.best = d_best; Q.count = d_count; Q.sum = d_sum;
+    const unsigned blocks = (unsigned)((Q.n + 255) / 256);
+    for (int64_t t = 0; t < n_gens; t++) {
+      const int par = (h->cur + (int)(t & 1)) & 1;
+      Q.pop = par ? h->P.pop1 : h->P.pop0;
+      Q.nxt = par ? h->P.pop0 : h->P.pop1;
+      Q.g = g0 + t; Q.t = t;
+      k_gaw_fitness<<<blocks, 256, 0, st>>>(Q);
+      size_t tb = h->scan_bytes;
+      CK(cub::DeviceScan::InclusiveSum(h->scan_tmp, tb, h->fw, h->cdfw, (int)Q.n, st));
+      k_gaw_children<<<blocks, 256, 0, st>>>(Q);
+    }
+    CK(cudaGetLastError());
+    g_launch[0] = 4; g_launch[1] = blocks; g_launch[2] = 256; g_launch[3] = 0; g_launch[4] = 3 * n_gens;
+    unsigned long long done = 0;
+    int32_t fl[2];
+    CK(cudaMemcpyAsync(&done, h->donew, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(fl, h->flags, 8, cudaMemcpyDeviceToHost, st));
+    if (best) CK(cudaMemcpyAsync(best, d_best, n_gens * 4, cudaMemcpyDefault, st));
+    if (count) CK(cudaMemcpyAsync(count, d_count, n_gens * 4, cudaMemcpyDefault, st));
+    if (sum) CK(cudaMemcpyAsync(sum, d_sum, n_gens * 8, cudaMemcpyDefault, st));
+    CK(cudaStreamSynchronize(st));
+    // current buffer: the generation the run stopped on, else the one after the last
+    const int64_t last = fl[0] ? (int64_t)(done - 1) : n_gens;
+    h->cur = (h->cur + (int)(last & 1)) & 1;
+    if (gens_done) *gens_done = (int64_t)done;
+    return 0;
+  }
   GaParams P = h->P;
   if (h->cur) std::swap(P.pop0, P.pop1);
   P.seed = seed; P.g0 = g0; P.n_gens = n_gens; P.target = target; P.adapt_count = adapt_count;
@@ -1213,11 +1318,37 @@ int tv_ga_replicas(int64_t n, int32_t L, int32_t mode, const uint64_t *T, int32_
   return 0;
 }
 
+int tv_ga_mutate(uint64_t *pop, int64_t n, int32_t L, const uint64_t *T, uint64_t pthr, int32_t method,
+                 uint64_t seed, int64_t g, uint64_t *flips, void *stream) {
+  NvtxRange nvtx_(method ? "tv_ga_mutate bitwise" : "tv_ga_mutate distribution", (long long)n);
+  if (!pop || !is_device_ptr(pop)) return fail(TV_ERR_ARG, "population must be a device pointer");
+  if (n < 1 || L < 1 || L > 64 * kGaMaxWords) return fail(TV_ERR_ARG, "n / L out of range");
+  if (method != 0 && method != 1) return fail(TV_ERR_ARG, "method must be 0 (distribution) or 1 (bit by bit)");
+  cudaStream_t st = (cudaStream_t)stream;
+  Scratch S(st);
+  uint64_t *Td = nullptr;
+  if (method == 0) {
+    if (is_device_ptr(T)) Td = const_cast<uint64_t *>(T);
+    else { CK(S.get(&Td, (size_t)L)); CK(cudaMemcpyAsync(Td, T, (size_t)L * 8, cudaMemcpyHostToDevice, st)); }
+  }
+  unsigned long long *fd = nullptr;
+  if (flips) { CK(S.get(&fd, 1)); CK(cudaMemsetAsync(fd, 0, 8, st)); }
+  k_ga_mutate<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(reinterpret_cast<unsigned long long *>(pop), n, L, Td,
+                                                            pthr, method, seed, g, fd);
+  CK(cudaGetLastError());
+  if (flips) {
+    CK(cudaMemcpyAsync(flips, fd, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  return 0;
+}
+
 int tv_ga_fitness_jatam(tv_ga *h, int32_t a, int32_t bpl, const int64_t *mask_pos, const uint8_t *mask_val,
                         int64_t m, const int64_t *free_pos, int64_t nfree, int32_t d, int32_t k, uint64_t seed,
                         int32_t strict, const uint8_t *target_occ, uint32_t *f_out, void *stream) {
   NvtxRange nvtx_("tv_ga_fitness_jatam");
   if (!h) return fail(TV_ERR_ARG, "null GA");
+  if (h->W > 1) return fail(TV_ERR_ARG, "JaTAM fitness needs L <= 64");
   if (d > 29) return fail(TV_ERR_ARG, "JaTAM fitness supports d <= 29");
   if (nfree != h->P.L) return fail(TV_ERR_ARG, "GA genome length %d != %lld free bits", h->P.L, (long long)nfree);
   if ((uint64_t)d * d * (uint64_t)h->P.n >= ((uint64_t)1 << 32)) return fail(TV_ERR_ARG, "d^2 * population must be < 2^32");

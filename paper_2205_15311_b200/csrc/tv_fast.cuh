@@ -237,16 +237,15 @@ template <typename M, int NC, bool STRICT> struct CandSwar {
     }
     uint32_t S = FM[0];  // the seed (no bonded side) shows all four faces
 #pragma unroll 1
-    for (int it = 0; it < 32; it++) {
-      uint32_t S2 = S;
+    for (int it = 0; it < 32; it++) {  // in-place (Gauss-Seidel) rounds: S only grows, so any order
+      const uint32_t S0 = S;           // reaches the same least fixpoint, in fewer rounds
 #pragma unroll
       for (int c = 0; c < NC; c++) {
         const uint32_t nzb = nz_byte(PM[c] & S);  // sides through which c can bond
         const uint32_t excl = (nzb & (nzb - 1u)) == 0u ? __funnelshift_l(nzb, nzb, 16) : 0u;
-        S2 |= nzb ? FM[c] & ~((excl >> 7) * 0xFFu) : 0u;
+        S |= nzb ? FM[c] & ~((excl >> 7) * 0xFFu) : 0u;
       }
-      if (S2 == S) break;
-      S = S2;
+      if (S == S0) break;
     }
     // pair test, SWAR over c2 for each c1 (nibble flags bit 4c+3): BK[k] = candidates that
     // bond through side k, ZK[k] = zero face at side k, SK = same face as c1 at side k

@@ -539,3 +539,201 @@ __global__ void __launch_bounds__(1024, 1) k_ga_replicas(const __grid_constant__
 }
 
 }  // namespace tvb
+
+namespace tvb {
+
+// ---------------------------------------------------------------------------
+// Wide genomes (64 < L <= 4096): W = ceil(L/64) words per genome, stored word-major on
+// the device (word w of genome i at pop[w * n + i], so every per-word access of a warp
+// is coalesced), little-endian words of genome.to_int() (genome position p = integer bit
+// L-1-p).  Semantics: oracle/tv_ga_oracle.c orc_ga_child_w / orc_ga_run_w (the narrow
+// operators with the uniform-crossover mask drawn one word at a time).  Per generation
+// three stream-ordered launches (fitness + stats, 64-bit inclusive CDF by CUB scan,
+// children); a device flag turns the launches of generations after a met stop
+// condition into no-ops, so a whole call is enqueued without host round trips.
+constexpr int kGaMaxWords = 64;  // L <= 4096
+
+struct GaWideParams {
+  int64_t n;
+  int32_t L, W, mode;
+  uint32_t target;
+  int64_t adapt_count;
+  int32_t stop_when;
+  uint64_t seed;
+  int64_t g;                      // generation index of this launch (g0 + t)
+  int64_t t;                      // stats row
+  const uint64_t *T;              // L Poisson thresholds (device)
+  const unsigned long long *pop;  // W x n (word-major)
+  unsigned long long *nxt;        // W x n
+  unsigned long long *f;          // n fitness (64-bit: the scan input)
+  unsigned long long *cdf;        // n inclusive CDF
+  uint32_t *best;                 // stats rows
+  unsigned long long *sum;
+  uint32_t *count;
+  int32_t *stopped;               // set once a stop condition is met
+  int32_t *final_par;             // parity (t & 1) of the generation the run stopped on, -1 = none
+  unsigned long long *done;       // generations evaluated
+};
+
+__device__ __forceinline__ uint64_t gw_full(int L, int w) {
+  const int hi = L - 64 * w;
+  return hi >= 64 ? ~0ULL : ((1ULL << hi) - 1);
+}
+
+__global__ void __launch_bounds__(256) k_gaw_fitness(const __grid_constant__ GaWideParams P) {
+  if (*((volatile int32_t *)P.stopped)) return;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t f = 0;
+  if (i < P.n) {
+    for (int w = 0; w < P.W; w++) f += (uint32_t)__popcll(P.pop[(int64_t)w * P.n + i]);
+    P.f[i] = f;
+  }
+  const bool in = i < P.n;
+  const uint32_t s = __reduce_add_sync(0xFFFFFFFFu, in ? f : 0u), mx = __reduce_max_sync(0xFFFFFFFFu, f);
+  const uint32_t nc = (uint32_t)__popc(__ballot_sync(0xFFFFFFFFu, in && f >= P.target));
+  if ((threadIdx.x & 31) == 0) {
+    if (s) atomicAdd(&P.sum[P.t], (unsigned long long)s);
+    if (mx) atomicMax(&P.best[P.t], mx);
+    if (nc) atomicAdd(&P.count[P.t], nc);
+  }
+  if (i == 0) *P.done = (unsigned long long)(P.t + 1);
+}
+
+// first j with cdf[j] > r (cdf[n-1] = total > r), or r itself scaled to n when total == 0
+__device__ __forceinline__ int64_t gw_select(const GaWideParams &P, uint64_t &s, uint64_t total) {
+  const uint64_t x = ga_draw(s);
+  if (total == 0) return (int64_t)__umul64hi(x, (uint64_t)P.n);
+  const uint64_t r = __umul64hi(x, total);
+  int64_t lo = 0, hi = P.n - 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (P.cdf[mid] > r) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(256) k_gaw_children(const __grid_constant__ GaWideParams P) {
+  if (*((volatile int32_t *)P.stopped)) return;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // stop after recording this generation's stats (evaluated before reproduction)
+  const uint32_t c = *((volatile uint32_t *)&P.count[P.t]);
+  if ((P.stop_when == 1 && c >= 1u) || (P.stop_when == 2 && (int64_t)c >= P.adapt_count)) {
+    __syncthreads();
+    if (i == 0) { *P.stopped = 1; *P.final_par = (int32_t)(P.t & 1); }
+    return;
+  }
+  if (i >= P.n) return;
+  const int L = P.L, W = P.W;
+  const uint64_t total = P.cdf[P.n - 1];
+  uint64_t s = stream_state(P.seed, (uint64_t)P.g, (uint64_t)i);
+  const int64_t a = gw_select(P, s, total);
+  int64_t b = a;
+  uint32_t pcut = 0;
+  uint64_t smask = 0;
+  if (P.mode != 0) {
+    b = gw_select(P, s, total);
+    if (P.mode == 1) pcut = __umulhi((uint32_t)(ga_draw(s) >> 32), (uint32_t)L);
+    else { smask = s; s += (uint64_t)W * kGold; }  // W mask draws, regenerated per word below
+  }
+  const uint64_t u = ga_draw(s) >> 1;
+  int k = 0;
+  while (k < L && u >= P.T[k]) k++;
+  uint64_t chosen[kGaMaxWords];
+  for (int w = 0; w < W; w++) chosen[w] = 0;
+  for (int fl = 0; fl < k;) {
+    const uint32_t p = __umulhi((uint32_t)(ga_draw(s) >> 32), (uint32_t)L);
+    const int bit = L - 1 - (int)p;
+    if ((chosen[bit >> 6] >> (bit & 63)) & 1ULL) continue;
+    chosen[bit >> 6] |= 1ULL << (bit & 63);
+    fl++;
+  }
+  const int lo = L - (int)pcut;  // single point: integer bits >= lo come from a
+  for (int w = 0; w < W; w++) {
+    const uint64_t full = gw_full(L, w);
+    const uint64_t av = P.pop[(int64_t)w * P.n + a];
+    uint64_t cv = av;
+    if (P.mode == 1) {
+      const uint64_t top = (lo <= 64 * w) ? ~0ULL : (lo >= 64 * w + 64) ? 0ULL : ~((1ULL << (lo - 64 * w)) - 1);
+      cv = (av & top) | (P.pop[(int64_t)w * P.n + b] & ~top);
+    } else if (P.mode == 2) {
+      const uint64_t m = mix64(smask + (uint64_t)(w + 1) * kGold) & full;
+      cv = (av & ~m) | (P.pop[(int64_t)w * P.n + b] & m);
+    }
+    P.nxt[(int64_t)w * P.n + i] = (cv ^ chosen[w]) & full;
+  }
+}
+
+// genome-major (host layout [n, W]) <-> word-major (device layout [W, n])
+__global__ void k_gaw_transpose(const unsigned long long *src, unsigned long long *dst, int64_t n, int32_t W,
+                                int32_t to_word_major) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n * W) return;
+  const int64_t i = j / W, w = j % W;
+  if (to_word_major) dst[w * n + i] = src[j];
+  else dst[j] = src[w * n + i];
+}
+
+// SPEC ACCEPTANCE 8 mutation benchmark (oracle/tv_ga_oracle.c orc_ga_mutate): genome i of a
+// word-major population mutated in place with stream (seed, g, i); method 0 = by
+// distribution (the GA's operator: only the touched words are read and written), 1 = bit by
+// bit (one draw per bit against the 64-bit threshold pthr, every word rewritten).
+__global__ void __launch_bounds__(256) k_ga_mutate(unsigned long long *pop, int64_t n, int32_t L,
+                                                   const uint64_t *T, uint64_t pthr, int32_t method, uint64_t seed,
+                                                   int64_t g, unsigned long long *flips) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t nf = 0;
+  if (i < n) {
+    uint64_t s = stream_state(seed, (uint64_t)g, (uint64_t)i);
+    if (method == 0) {
+      const uint64_t u = ga_draw(s) >> 1;
+      int k = 0;
+      while (k < L && u >= T[k]) k++;
+      // distinct positions by rejection; k is small (lambda = muL), so a short list suffices
+      // for the membership test, with a bitset fallback for large k
+      int pos[16];
+      uint64_t chosen[kGaMaxWords];
+      const bool small = k <= 16;
+      if (!small)
+        for (int w = 0; w < (L + 63) / 64; w++) chosen[w] = 0;
+      for (int fl = 0; fl < k;) {
+        const uint32_t p = __umulhi((uint32_t)(ga_draw(s) >> 32), (uint32_t)L);
+        const int bit = L - 1 - (int)p;
+        bool dup = false;
+        if (small) {
+          for (int j = 0; j < fl; j++) dup |= pos[j] == bit;
+          if (dup) continue;
+          pos[fl] = bit;
+        } else {
+          if ((chosen[bit >> 6] >> (bit & 63)) & 1ULL) continue;
+          chosen[bit >> 6] |= 1ULL << (bit & 63);
+        }
+        fl++;
+      }
+      if (small) {
+        for (int j = 0; j < k; j++) pop[(int64_t)(pos[j] >> 6) * n + i] ^= 1ULL << (pos[j] & 63);
+      } else {
+        for (int w = 0; w < (L + 63) / 64; w++)
+          if (chosen[w]) pop[(int64_t)w * n + i] ^= chosen[w];
+      }
+      nf = (uint32_t)k;
+    } else {
+      const int W = (L + 63) / 64;
+      for (int w = W - 1; w >= 0; w--) {  // bit L-1-p lies in word (L-1-p) >> 6: p ascending = words descending
+        uint64_t m = 0;
+        const int b_hi = min(63, L - 1 - 64 * w);
+        for (int b = b_hi; b >= 0; b--) {  // p = L-1-(64w+b) ascending
+          const bool fl = ga_draw(s) < pthr;
+          m |= (uint64_t)fl << b;
+          nf += fl;
+        }
+        pop[(int64_t)w * n + i] ^= m;
+      }
+    }
+  }
+  if (flips) {
+    const uint32_t tot = __reduce_add_sync(0xFFFFFFFFu, nf);
+    if ((threadIdx.x & 31) == 0 && tot) atomicAdd(flips, (unsigned long long)tot);
+  }
+}
+
+}  // namespace tvb

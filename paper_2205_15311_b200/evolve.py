@@ -12,7 +12,11 @@ geometry; the CPU restatement oracle/tv_ga_oracle.c reproduces it bit for bit
 with the same draw semantics (they are what one child of the kernel does).
 
 Genomes are held as the integer ``Genome.to_int()`` (genome bit 0 = most
-significant of L bits); L <= 64.
+significant of L bits).  L <= 64: one u64 per genome and the cooperative
+kernel; 64 < L <= 4096: ``W = ceil(L/64)`` little-endian u64 words per genome
+(arrays ``[n, W]``, word 0 = the integer's low 64 bits), three launches per
+generation (oracle/tv_ga_oracle.c ``orc_ga_run_w``; the uniform-crossover mask is
+drawn one word at a time, word 0 first, which for W = 1 is the narrow operator).
 """
 from __future__ import annotations
 
@@ -124,7 +128,9 @@ def crossover_uniform(a, b, rng: GaRng, L: int | None = None):
     if la is not None and la != lb:
         raise ValueError("genome lengths differ")
     L = L or la
-    m = rng.next() & ((1 << L) - 1)
+    m = 0
+    for w in range((L + 63) // 64):  # one draw per 64-bit word, word 0 (the low bits) first
+        m |= (rng.next() & ((1 << min(64, L - 64 * w)) - 1)) << (64 * w)
     out = (av & ~m) | (bv & m)
     return Genome.from_int(L, out) if la else out
 
@@ -214,6 +220,7 @@ class DeviceGA:
 
     def __init__(self, pop_size: int, length: int, mu_L: float, mode: str = "asexual"):
         self.n, self.L = int(pop_size), int(length)
+        self.W = (self.L + 63) // 64  # words per genome (> 1: the wide path, arrays [n, W])
         self.mode = MODES[mode] if isinstance(mode, str) else int(mode)
         self.T = poisson_thresholds(mu_L, self.L)
         h = ctypes.c_void_p()
@@ -233,11 +240,16 @@ class DeviceGA:
             pass
 
     def set_population(self, genomes=None):
-        g = None if genomes is None else np.ascontiguousarray(genomes, np.uint64)
+        g = None
+        if genomes is not None:
+            g = np.ascontiguousarray(genomes, np.uint64)
+            want = (self.n,) if self.W == 1 else (self.n, self.W)
+            if g.shape != want:
+                raise ValueError(f"population must have shape {want}, got {g.shape}")
         _lib.check(_lib.lib().tv_ga_set_population(self._h, _lib.ptr(g), None))
 
     def population(self) -> np.ndarray:
-        out = np.empty(self.n, np.uint64)
+        out = np.empty(self.n if self.W == 1 else (self.n, self.W), np.uint64)
         _lib.check(_lib.lib().tv_ga_get_population(self._h, _lib.ptr(out), None))
         return out
 
@@ -364,6 +376,8 @@ def run_replicas(cfg: GAConfig, seeds) -> list[RunRecord]:
     R, n, L = seeds.shape[0], int(cfg.pop_size), int(cfg.length)
     if R == 0:
         return []
+    if L > 64:  # replica kernel holds one u64 per genome: wide runs go one launch sequence each
+        return [run_ga(cfg, seed=int(x)) for x in seeds]
     if n > REPLICA_MAX_POP:
         raise ValueError(f"replica runs hold the population in shared memory: pop_size <= {REPLICA_MAX_POP}")
     T = poisson_thresholds(cfg.mu_L, L)
@@ -459,3 +473,60 @@ def write_trace_csv(record: RunRecord, path_or_buf=None) -> str:
             with open(path_or_buf, "w") as f:
                 f.write(text)
     return text
+
+
+def bernoulli_threshold(mu_L: float, L: int) -> int:
+    """64-bit threshold of bit-by-bit mutation: a bit flips when its draw < floor(p * 2^64), p = mu_L / L."""
+    p = min(1.0, max(0.0, mu_L / L))
+    return min((1 << 64) - 1, int(math.floor(p * 2.0 ** 64)))
+
+
+def mutate_population(pop, L: int, mu_L: float, method: str = "distribution", seed: int = 0, g: int = 0,
+                      count_flips: bool = False, stream=None, T=None):
+    """Mutate a device population in place (tv_ga_mutate).  ``pop`` is a CUDA tensor of
+    ``W * n`` u64 words, word-major (word w of genome i at ``w * n + i``); method
+    "distribution" = the GA's operator (k ~ Poisson(mu_L) distinct flips), "bitwise" = one
+    draw per bit (SPEC ACCEPTANCE 8's baseline).  ``T``: precomputed thresholds (host array
+    or CUDA tensor), else computed here.  Returns the flip count if asked."""
+    W = (L + 63) // 64
+    n = pop.numel() // W
+    if T is None:
+        T = poisson_thresholds(mu_L, L)
+    flips = np.zeros(1, np.uint64) if count_flips else None
+    m = {"distribution": 0, "bitwise": 1}[method]
+    _lib.check(_lib.lib().tv_ga_mutate(_lib.ptr(pop), n, L, _lib.ptr(T), bernoulli_threshold(mu_L, L), m,
+                                       int(np.uint64(seed)), int(g), _lib.ptr(flips), stream))
+    return int(flips[0]) if count_flips else None
+
+
+def mutation_benchmark(pop_size: int = 1 << 20, length: int = 1024, mu_L: float = 0.5, reps: int = 5,
+                       seed: int = 0) -> dict:
+    """SPEC ACCEPTANCE 8 (Fig. 5's regime): device time per generation of mutating a
+    population of ``length``-bit genomes by distribution (the GA operator) vs bit by bit,
+    CUDA events on the launch stream, best of ``reps``."""
+    import torch
+    W = (length + 63) // 64
+    pop = torch.zeros(W * pop_size, dtype=torch.int64, device="cuda")
+    st = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(st.cuda_stream)
+    Td = torch.from_numpy(poisson_thresholds(mu_L, length).view(np.int64)).cuda()  # no host work in the timed region
+    out = {}
+    gens = 20  # launches per timed region (back to back, one generation each)
+    for method in ("distribution", "bitwise"):
+        mutate_population(pop, length, mu_L, method, seed, 0, stream=sp, T=Td)  # warm-up
+        best = float("inf")
+        for r in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(st)
+            for j in range(gens):
+                mutate_population(pop, length, mu_L, method, seed, 1 + r * gens + j, stream=sp, T=Td)
+            e1.record(st)
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1) / gens)
+        out[method + "_ms"] = best
+        out[method + "_flips_per_genome"] = mutate_population(pop, length, mu_L, method, seed, 99,
+                                                              count_flips=True, stream=sp, T=Td) / pop_size
+    out["speedup"] = out["bitwise_ms"] / out["distribution_ms"]
+    out.update(pop_size=pop_size, length=length, mu_L=mu_L)
+    return out

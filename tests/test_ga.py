@@ -354,3 +354,117 @@ def test_jatam_generations_external_fitness_vs_restatement(mode):
         pop = ga.population()
         assert np.array_equal(pop, exp), g
     ga.close()
+
+
+# ---------------------------------------------------------------- wide genomes (L > 64)
+def _wide_random(rng, n, L):
+    W = (L + 63) // 64
+    pop = rng.integers(0, 2**63, (n, W), dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, (n, W), dtype=np.uint64)
+    if L % 64:
+        pop[:, W - 1] &= np.uint64((1 << (L % 64)) - 1)
+    return np.ascontiguousarray(pop)
+
+
+@pytest.mark.parametrize("L,mode", [(20, 0), (32, 1), (64, 2), (47, 2), (64, 1)])
+def test_wide_restatement_equals_narrow_at_one_word(L, mode):
+    """orc_ga_run_w with W = 1 is the narrow restatement (same draws, same children, same stats)."""
+    rng = np.random.default_rng(L + mode)
+    pop = _wide_random(rng, 300, L)[:, 0].copy()
+    pop[::3] = 0
+    wide = pop[:, None].copy()
+    T = E.poisson_thresholds(1.5, L)
+    a = O.ga_run(pop, L, mode, T, 5, 0, 30, L // 2, 150, 0)
+    b = O.ga_run_w(wide, L, mode, T, 5, 0, 30, L // 2, 150, 0)
+    assert a[0] == b[0] and all(np.array_equal(x, y) for x, y in zip(a[1:], b[1:]))
+    assert np.array_equal(pop, wide[:, 0])
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_wide_host_operators_equal_restatement(mode):
+    """The host single-genome operators on Python ints (any L) compose the wide child."""
+    L, W = 150, 3
+    rng = np.random.default_rng(mode)
+    pop = _wide_random(rng, 29, L)
+    pop[::4] = 0
+    ints = [sum(int(pop[i, w]) << (64 * w) for w in range(W)) for i in range(pop.shape[0])]
+    cdf = np.cumsum([bin(v).count("1") for v in ints]).astype(np.uint64)
+    T = E.poisson_thresholds(2.0, L)
+    for i in range(30):
+        r = E.GaRng(3, 7, i)
+        wts = np.array([bin(v).count("1") for v in ints], np.int64)
+        child = ints[E.roulette_select(wts, r)]
+        if mode:
+            b = ints[E.roulette_select(wts, r)]
+            child = E.crossover_single_point(child, b, r, L) if mode == 1 else E.crossover_uniform(child, b, r, L)
+        child = E.mutate(child, 2.0, r, L)
+        got = O.ga_child_w(3, 7, i, pop, cdf, L, mode, T)
+        assert child == sum(int(got[w]) << (64 * w) for w in range(W)), i
+
+
+def test_mutation_benchmark_operators_restatement():
+    """ACCEPTANCE 8 operators on the CPU: the distribution method flips Poisson(muL) distinct bits,
+    bit by bit flips Binomial(L, muL / L); both have mean muL."""
+    L, n, mu = 1024, 20000, 0.5
+    T = E.poisson_thresholds(mu, L)
+    for method in (0, 1):
+        pop = np.zeros((n, 16), np.uint64)
+        flips = O.ga_mutate(pop, L, T, E.bernoulli_threshold(mu, L), method, 1, 0)
+        pc = sum(bin(int(x)).count("1") for x in pop.reshape(-1)[pop.reshape(-1) != 0])
+        assert pc == flips  # distinct positions on an all-zero population
+        assert abs(flips / n - mu) < 5 * math.sqrt(mu / n), (method, flips / n)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("L,mode,lam,stop", [(65, 0, 0.3, 0), (100, 1, 1.0, 0), (128, 2, 2.0, 0), (1024, 0, 0.5, 0),
+                                             (1000, 2, 4.0, 0), (200, 0, 3.0, 1)])
+def test_wide_device_ga_equals_restatement(L, mode, lam, stop):
+    n = 3001
+    ga = E.DeviceGA(n, L, lam, mode)
+    rng = np.random.default_rng(L)
+    init = _wide_random(rng, n, L)
+    init[: n // 2] = 0
+    ga.set_population(init)
+    assert np.array_equal(ga.population(), init)
+    pop = init.copy()
+    T = E.poisson_thresholds(lam, L)
+    tgt = int(0.55 * L) if stop else L // 2
+    g = 0
+    for chunk in (7, 13):
+        k, b, s, c = ga.run(21, g, chunk, tgt, n // 2, stop)
+        k2, b2, s2, c2 = O.ga_run_w(pop, L, mode, T, 21, g, chunk, tgt, n // 2, stop)
+        assert k == k2 and np.array_equal(b, b2) and np.array_equal(s, s2) and np.array_equal(c, c2)
+        assert np.array_equal(ga.population(), pop), (g, k)
+        g += k
+    ga.close()
+
+
+@pytest.mark.gpu
+def test_wide_run_ga_public_api():
+    cfg = E.GAConfig(pop_size=2048, length=256, mu_L=1.0, cutoff=60, target=140, stop_when="discovery")
+    rec = E.run_ga(cfg, seed=4)
+    pop = np.zeros((2048, 4), np.uint64)
+    k, b, s, c = O.ga_run_w(pop, 256, 0, E.poisson_thresholds(1.0, 256), 4, 0, 60, 140, 1024, 1)
+    assert rec.generations == k and np.array_equal(rec.best, b) and np.array_equal(rec.count_at_target, c)
+    assert len(E.run_replicas(E.GAConfig(pop_size=256, length=100, cutoff=5, stop_when="never"), [1, 2])) == 2
+
+
+@pytest.mark.gpu
+def test_mutation_benchmark_device_equals_restatement_and_speedup():
+    """SPEC ACCEPTANCE 8: mutation by distribution beats bit-by-bit flipping by >= 2x at
+    L = 1024, muL = 0.5 (device, bench.py's mutation_L1024 line); both device operators equal
+    the CPU restatement bit for bit."""
+    import torch
+    L, n, mu = 1024, 4096, 0.5
+    W = L // 64
+    for method in ("distribution", "bitwise"):
+        dev = torch.zeros(W * n, dtype=torch.int64, device="cuda")
+        f = E.mutate_population(dev, L, mu, method, seed=3, g=2, count_flips=True)
+        host = np.zeros((n, W), np.uint64)
+        f2 = O.ga_mutate(host, L, E.poisson_thresholds(mu, L), E.bernoulli_threshold(mu, L),
+                         0 if method == "distribution" else 1, 3, 2)
+        assert f == f2
+        got = dev.cpu().numpy().view(np.uint64).reshape(W, n).T
+        assert np.array_equal(got, host), method
+    r = E.mutation_benchmark(pop_size=1 << 18, length=1024, mu_L=0.5, reps=3)
+    assert r["speedup"] >= 2.0, r
+    assert abs(r["distribution_flips_per_genome"] - 0.5) < 0.02 and abs(r["bitwise_flips_per_genome"] - 0.5) < 0.02
