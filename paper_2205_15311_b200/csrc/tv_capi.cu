@@ -185,9 +185,11 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
     // parked lanes that trigger a service pass (measured: a = 2 best at 14 after the round-2 work
     // elimination, 18.62 vs 18.82 ms at 12; a = 3 at 16-20)
     P.service_thresh = et ? atoi(et) : (P.a == 3 ? 20 : 14);
-    // locally-forced run-0 assemblies end the genome DET after one run (TV_FORCED=0 disables)
+    // locally-forced run-0 assemblies end the genome DET after one run (TV_FORCED=0 disables).
+    // a = 3 checks only provably trivial-free genomes (2): the 64-bit check costs about what it
+    // saves on the others (S32 2^24 block 24.27 -> 24.03 ms); a <= 2 checks all (S28 18.5 vs 19.5 ms)
     const char *efz = getenv("TV_FORCED");
-    P.forced_check = efz ? (atoi(efz) != 0) : 1;
+    P.forced_check = efz ? std::max(0, std::min(2, atoi(efz))) : (P.a == 3 ? 2 : 1);
     // per-CTA phenotype cache: 256 slots (with the behaviour-sorted order a CTA sees many
     // phenotypes of alike genomes: S28 32.3 -> 31.6 ms vs 128 slots; 512 halves occupancy)
     P.cta_slots = P.hist_mode ? (ec ? atoi(ec) : 256) : 0;

@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
         int w = 0, h = 0, n = 0, ov = 0;
         const bool fit_scan = P.fit_mode && !replay && run == 0;  // overlap with the GA target shape
         // run 0 of a genome: is its assembly locally forced (every run must reproduce it)?
-        bool forced = P.forced_check && !replay && !P.pay_mode && run == 0;
+        bool forced = P.forced_check && (P.forced_check == 1 || tfree) && !replay && !P.pay_mode && run == 0;
         if (ended == RUN_BOUNDED) {
           unsigned long long *out = nullptr;
           int64_t W = 0;

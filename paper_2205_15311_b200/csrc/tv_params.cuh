@@ -51,6 +51,7 @@ struct ClassifyParams {
   int32_t cta_slots;        // fast kernel: per-CTA shared histogram slots (power of 2; 0 = off)
   int32_t service_thresh;   // fast kernel: parked lanes that trigger a warp service pass (0 = default)
   int32_t forced_check;     // fast kernel: skip runs 1.. of genomes whose run-0 assembly is locally forced
+                            // (1: check every genome, 2: only provably trivial-free ones)
   const uint32_t *tf_flags; // fast kernel: per-item trivial-freedom bits (early unbound cut-off), or nullptr
   const uint32_t *order;    // fast kernel, histogram mode: work-item permutation (k_prepass sort), or nullptr
   const unsigned long long *n_skip;  // fast kernel: the last *n_skip order entries (1-mers) are done, or nullptr

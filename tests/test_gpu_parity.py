@@ -184,7 +184,7 @@ def test_enumerate_generic_path_histogram(K):
 # UNBOUND run of a provably trivial-free genome), TV_ONEMER (1-mers classified by the
 # pre-pass), TV_FORCED (stop after run 0 when its assembly is locally forced).  Results must
 # be identical under every combination.
-SWITCHES = [(0, 0, 0), (1, 1, 1), (1, 0, 0), (0, 1, 0), (0, 0, 1)]
+SWITCHES = [(0, 0, 0), (1, 1, 1), (1, 0, 0), (0, 1, 0), (0, 0, 1), (1, 1, 2)]
 
 
 @pytest.fixture

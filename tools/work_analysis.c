@@ -172,10 +172,10 @@ int main(int argc, char **argv) {
     uint64_t tot_pops = 0, tot_runs = 0, om_g = 0, om_pops = 0, om_runs = 0;
     uint64_t au_pops = 0, au_fu_pops = 0, au_fu_tf_pops = 0, au_tr_pops = 0, au_fu_g = 0, au_fu_tf_g = 0;
     uint64_t unb_g = 0, tf_g = 0, tf2_g = 0, au_fu_tf2_pops = 0, au_fu_tf2_g = 0, viol2 = 0, au_runs = 0, au_fu_runs = 0, au_fu_tf_runs = 0;
-    uint64_t ex_cls[4] = {0, 0, 0, 0}, ex_runs_cls[4] = {0, 0, 0, 0}, ops_ref = 0, ops_exec = 0, runs_exec = 0, pops_exec = 0, fz_g = 0, fz_pops_saved = 0, fz_runs_saved = 0, fz_viol = 0, fz_det = 0, run0_unb_pops = 0, cls[4] = {0, 0, 0, 0}, cls_pops[4] = {0, 0, 0, 0}, det_tf2_pops = 0, det_tf2_g = 0;
+    uint64_t hist_exec[8] = {0}, fz_not_tf = 0, fz_not_tf_runs = 0, b0_checked_not_tf = 0, ex_cls[4] = {0, 0, 0, 0}, ex_runs_cls[4] = {0, 0, 0, 0}, ops_ref = 0, ops_exec = 0, runs_exec = 0, pops_exec = 0, fz_g = 0, fz_pops_saved = 0, fz_runs_saved = 0, fz_viol = 0, fz_det = 0, run0_unb_pops = 0, cls[4] = {0, 0, 0, 0}, cls_pops[4] = {0, 0, 0, 0}, det_tf2_pops = 0, det_tf2_g = 0;
 #pragma omp parallel reduction(+ : tot_pops, tot_runs, om_g, om_pops, om_runs, au_pops, au_fu_pops, au_fu_tf_pops, \
                                au_tr_pops, au_fu_g, au_fu_tf_g, unb_g, tf_g, au_runs, au_fu_runs, au_fu_tf_runs, \
-                               ex_cls[:4], ex_runs_cls[:4], ops_ref, ops_exec, runs_exec, pops_exec, fz_g, fz_pops_saved, fz_runs_saved, fz_viol, fz_det, run0_unb_pops, cls[:4], cls_pops[:4], det_tf2_pops, det_tf2_g, tf2_g, au_fu_tf2_pops, au_fu_tf2_g, viol2)
+                               hist_exec[:8], fz_not_tf, fz_not_tf_runs, b0_checked_not_tf, ex_cls[:4], ex_runs_cls[:4], ops_ref, ops_exec, runs_exec, pops_exec, fz_g, fz_pops_saved, fz_runs_saved, fz_viol, fz_det, run0_unb_pops, cls[:4], cls_pops[:4], det_tf2_pops, det_tf2_g, tf2_g, au_fu_tf2_pops, au_fu_tf2_g, viol2)
     {
         orc_scratch S;
         orc_scratch_alloc(&S, d);
@@ -242,6 +242,13 @@ int main(int argc, char **argv) {
                     if (r < ne) { ops_exec += o; runs_exec++; pops_exec += RC[r].pops; ex_cls[c] += RC[r].pops; ex_runs_cls[c]++; }
                 }
                 ops_ref += 64;
+                {   /* executed pops per genome, log2 buckets from 64 */
+                    uint64_t ep = 0;
+                    for (int r = 0; r < ne; r++) ep += RC[r].pops;
+                    int b = 0;
+                    while (b < 7 && ep >= (64ULL << b)) b++;
+                    hist_exec[b]++;
+                }
                 ops_exec += om ? 16 : 64;
             }
             if (one_mer(E, a)) { om_g++; om_pops += gp; om_runs += nr; }
@@ -250,6 +257,8 @@ int main(int argc, char **argv) {
             int tf2 = trivial_free_v2(E, a, strict);
             tf2_g += tf2;
             if (tf2 && c == 0) { det_tf2_g++; det_tf2_pops += gp; }
+            if (fz && !tf2 && !one_mer(E, a)) { fz_not_tf++; fz_not_tf_runs += nr - 1; }
+            if (outc[0] == ORC_RUN_BOUNDED && !tf2) b0_checked_not_tf++;
             if (tf2 && triv >= 0) viol2++;  /* unsound proof: a TRIVIAL it said impossible */
             if (first_unb == 0) run0_unb_pops += gp - pops[0];
             if (first_unb >= 0) {
@@ -297,6 +306,12 @@ int main(int argc, char **argv) {
     printf(" \"ops_per_genome_reference\": %.2f, \"ops_per_genome_executed\": %.2f, \"runs_executed\": %llu, \"pops_executed\": %llu,\n",
            (double)ops_ref / (double)count, (double)ops_exec / (double)count, (unsigned long long)runs_exec,
            (unsigned long long)pops_exec);
+    printf(" \"forced_not_tfree\": {\"genomes\": %llu, \"runs_saved\": %llu}, \"run0_bounded_not_tfree\": %llu,\n",
+           (unsigned long long)fz_not_tf, (unsigned long long)fz_not_tf_runs, (unsigned long long)b0_checked_not_tf);
+    printf(" \"executed_pops_per_genome_log2_buckets_from_64\": [%llu, %llu, %llu, %llu, %llu, %llu, %llu, %llu],\n",
+           (unsigned long long)hist_exec[0], (unsigned long long)hist_exec[1], (unsigned long long)hist_exec[2],
+           (unsigned long long)hist_exec[3], (unsigned long long)hist_exec[4], (unsigned long long)hist_exec[5],
+           (unsigned long long)hist_exec[6], (unsigned long long)hist_exec[7]);
     printf(" \"executed_pops_by_class\": [%llu, %llu, %llu, %llu], \"executed_runs_by_class\": [%llu, %llu, %llu, %llu],\n",
            (unsigned long long)ex_cls[0], (unsigned long long)ex_cls[1], (unsigned long long)ex_cls[2], (unsigned long long)ex_cls[3],
            (unsigned long long)ex_runs_cls[0], (unsigned long long)ex_runs_cls[1], (unsigned long long)ex_runs_cls[2], (unsigned long long)ex_runs_cls[3]);
