@@ -163,6 +163,22 @@ int fill_common(int32_t a, int32_t bpl, const int64_t *mask_pos, const uint8_t *
   return 0;
 }
 
+// k_classify_fast<A, STRICT, MODE> for runtime (a, strict, mode)
+template <int A, bool S> const void *fast_kernel_fn_m(int mode) {
+  switch (mode) {
+    case FM_HIST: return (const void *)k_classify_fast<A, S, FM_HIST>;
+    case FM_FIT: return (const void *)k_classify_fast<A, S, FM_FIT>;
+    case FM_PAY: return (const void *)k_classify_fast<A, S, FM_PAY>;
+    default: return (const void *)k_classify_fast<A, S, FM_ROWS>;
+  }
+}
+const void *fast_kernel_fn(int a, bool strict, int mode) {
+  if (strict) return a == 1 ? fast_kernel_fn_m<1, true>(mode) : a == 2 ? fast_kernel_fn_m<2, true>(mode)
+                                                                     : fast_kernel_fn_m<3, true>(mode);
+  return a == 1 ? fast_kernel_fn_m<1, false>(mode) : a == 2 ? fast_kernel_fn_m<2, false>(mode)
+                                                             : fast_kernel_fn_m<3, false>(mode);
+}
+
 // Launch the chosen kernel for P (n items, indices or range already set).
 int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
   ClassifyParams &P = C.P;
@@ -211,11 +227,8 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
       smem = fast_smem_bytes(threads, P.GW, P.S, P.cta_slots, P.q);
     }
     if (smem <= (size_t)maxsmem) {
-      const void *fn = P.strict
-          ? (P.a == 1 ? (const void *)k_classify_fast<1, true>
-             : P.a == 2 ? (const void *)k_classify_fast<2, true> : (const void *)k_classify_fast<3, true>)
-          : (P.a == 1 ? (const void *)k_classify_fast<1, false>
-             : P.a == 2 ? (const void *)k_classify_fast<2, false> : (const void *)k_classify_fast<3, false>);
+      const int mode = P.hist_mode ? FM_HIST : P.pay_mode ? FM_PAY : P.fit_mode ? FM_FIT : FM_ROWS;
+      const void *fn = fast_kernel_fn(P.a, P.strict != 0, mode);
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       int per_sm = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem));

@@ -241,9 +241,12 @@ template <typename M, int NC, bool STRICT> struct CandSwar {
       const uint32_t S0 = S;           // reaches the same least fixpoint, in fewer rounds
 #pragma unroll
       for (int c = 0; c < NC; c++) {
-        const uint32_t nzb = nz_byte(PM[c] & S);  // sides through which c can bond
-        const uint32_t excl = (nzb & (nzb - 1u)) == 0u ? __funnelshift_l(nzb, nzb, 16) : 0u;
-        S |= nzb ? FM[c] & ~((excl >> 7) * 0xFFu) : 0u;
+        // T: sides through which c can bond (bit 7 of byte j); c shows its face toward side k' iff
+        // it bonds through a side other than the opposite one, (k'+2)&3: OR of T's bytes k'-1,
+        // k', k'+1 = T | rotl8(T) | rotr8(T), spread to whole bytes
+        const uint32_t T = nz_byte(PM[c] & S);
+        const uint32_t A = T | __funnelshift_l(T, T, 8) | __funnelshift_r(T, T, 8);
+        S |= FM[c] & ((A >> 7) * 0xFFu);
       }
       if (S == S0) break;
     }
@@ -318,9 +321,14 @@ __host__ __device__ inline int fast_board_words(int a, int d) {
 #endif
 template <int A> constexpr int fast_threads() { return A == 3 ? TV_FAST_MAXT3 : TV_FAST_MAXT; }
 
-template <int A, bool STRICT>
+// MODE (compile time, so each variant carries only its own service code): 0 histogram,
+// 1 classify_batch rows, 2 GA fitness, 3 representative payloads (HIST / fit_mode / pay_mode)
+enum { FM_HIST = 0, FM_ROWS = 1, FM_FIT = 2, FM_PAY = 3 };
+
+template <int A, bool STRICT, int MODE>
 __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fast(const __grid_constant__ ClassifyParams P) {
   constexpr int NC = 4 * A;
+  constexpr bool HIST = MODE == FM_HIST, FIT = MODE == FM_FIT, PAY = MODE == FM_PAY;
   extern __shared__ uint32_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
@@ -343,7 +351,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
   uint32_t *c_ste = c_det + HS;
   int32_t *c_gs = reinterpret_cast<int32_t *>(c_ste + HS);
   uint32_t *c_tal = reinterpret_cast<uint32_t *>(c_gs + HS);
-  if (P.hist_mode) {
+  if (HIST) {
     for (int s = threadIdx.x; s < HS; s += blockDim.x) {
       c_key[s] = 0ULL; c_rdet[s] = ~0ULL; c_rany[s] = ~0ULL; c_det[s] = 0; c_ste[s] = 0; c_gs[s] = -1;
     }
@@ -387,15 +395,15 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
         // hash (+ pack on replay) the bounded shape before clearing (_k:260-292)
         uint32_t hs = 0;
         int w = 0, h = 0, n = 0, ov = 0;
-        const bool fit_scan = P.fit_mode && !replay && run == 0;  // overlap with the GA target shape
+        const bool fit_scan = FIT && !replay && run == 0;  // overlap with the GA target shape
         // run 0 of a genome: is its assembly locally forced (every run must reproduce it)?
-        bool forced = P.forced_check && (P.forced_check == 1 || tfree) && !replay && !P.pay_mode && run == 0;
+        bool forced = P.forced_check && (P.forced_check == 1 || tfree) && !replay && !PAY && run == 0;
         if (ended == RUN_BOUNDED) {
           unsigned long long *out = nullptr;
           int64_t W = 0;
-          if (replay || P.pay_mode) {
-            out = P.hist_mode ? P.hist.shape + pslot * P.hist.W : P.out_shape + item * P.W;
-            W = P.hist_mode ? P.hist.W : P.W;
+          if (replay || PAY) {
+            out = HIST ? P.hist.shape + pslot * P.hist.W : P.out_shape + item * P.W;
+            W = HIST ? P.hist.W : P.W;
           }
           w = maxc - minc + 1;
           h = maxr - minr + 1;
@@ -437,7 +445,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
           for (int wi = lo; wi <= hi; wi++) Ln.gw[wi * 32] = 0xFFFFFFFFu;
         }
         if (replay) {
-          if (!P.hist_mode) {
+          if (!HIST) {
             P.out_hash[item] = best;
             P.out_w[item] = (uint8_t)w; P.out_h[item] = (uint8_t)h; P.out_cells[item] = (uint16_t)n;
           } else {  // the genome that claimed the key provides its payload (fixed at export
@@ -446,7 +454,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
             P.hist.pay_idx[pslot] = idx;
           }
           st = ST_NEED;
-        } else if (P.pay_mode) {  // representative payload: does this run reproduce the key?
+        } else if (PAY) {  // representative payload: does this run reproduce the key?
           const uint32_t key = P.pay_key[item >> P.pay_shift];
           if (ended == RUN_BOUNDED && hs == key) {
             P.out_hash[item] = hs;
@@ -467,7 +475,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
               if (forced) done = true;
             }
             else if (first_mismatch < 0 && first_unbound != 0 && hs != hash0) first_mismatch = run;
-            if (P.fit_mode && first_mismatch >= 0) done = true;  // not DET: fitness 0 whatever follows
+            if (FIT && first_mismatch >= 0) done = true;  // not DET: fitness 0 whatever follows
           } else if (ended == RUN_UNBOUND) {
             rh[run * 32] = 0u;
             if (first_unbound < 0) {
@@ -476,7 +484,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
               // later run goes TRIVIAL, which the genome's flag proves impossible
               if (tfree) done = true;
             }
-            if (P.fit_mode) done = true;  // not DET: fitness 0 whatever follows
+            if (FIT) done = true;  // not DET: fitness 0 whatever follows
           } else {
             done = true;
             if (ended == RUN_TRIVIAL) trivial_at = run;
@@ -484,13 +492,13 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
           run++;
           if (!done && run < P.kmax) {
             start = true;
-          } else if (P.fit_mode) {  // GA JaTAM-shape fitness: d^2 - shapediff for DET, else 0
+          } else if (FIT) {  // GA JaTAM-shape fitness: d^2 - shapediff for DET, else 0
             const int hc = ended == RUN_OVERFLOW ? CLS_ERROR : class_at(P.hist_k, trivial_at, first_unbound, first_mismatch);
             const int diff = P.target_cells + (int)(fit0 & 0xFFFFu) - 2 * (int)(fit0 >> 16);
             P.out_fit[item] = hc == CLS_DET ? (uint32_t)(dd - diff) : 0u;
             st = ST_NEED;
           } else if (ended == RUN_OVERFLOW) {  // _k:434-437
-            if (!P.hist_mode) {
+            if (!HIST) {
               for (int k = 0; k < P.q; k++) P.out_class[item * P.q + k] = (uint8_t)CLS_ERROR;
             } else {
               for (int k = 0; k < P.q; k++) atomicAdd(&c_tal[k * 5 + 4], 1u);
@@ -498,7 +506,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
             st = ST_NEED;
           } else {
             // ---- genome fold (_k:351-381, _k:438-452)
-            if (!P.hist_mode) {
+            if (!HIST) {
               for (int k = 0; k < P.q; k++)
                 P.out_class[item * P.q + k] = (uint8_t)class_at(P.ks[k], trivial_at, first_unbound, first_mismatch);
             } else {
@@ -524,7 +532,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
                     if (rh[j * 32] == best) { attr = j; break; }
               }
               bool need_payload = true;
-              if (P.hist_mode) {
+              if (HIST) {
                 const bool det = hc == CLS_DET;
                 bool gnew = false, cached = false;
                 int64_t g = -1;
@@ -568,7 +576,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
                 start = true;
                 st = ST_RUN;
               }
-            } else if (!P.hist_mode) {
+            } else if (!HIST) {
               P.out_hash[item] = 0u; P.out_w[item] = 0; P.out_h[item] = 0; P.out_cells[item] = 0;
             }
           }
@@ -706,7 +714,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
     else if (sp == 0) pend = RUN_BOUNDED;
   }
 
-  if (P.hist_mode) {
+  if (HIST) {
     __syncthreads();
     for (int s = threadIdx.x; s < HS; s += blockDim.x) {
       if (c_key[s] == 0ULL) continue;

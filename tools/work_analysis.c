@@ -172,10 +172,10 @@ int main(int argc, char **argv) {
     uint64_t tot_pops = 0, tot_runs = 0, om_g = 0, om_pops = 0, om_runs = 0;
     uint64_t au_pops = 0, au_fu_pops = 0, au_fu_tf_pops = 0, au_tr_pops = 0, au_fu_g = 0, au_fu_tf_g = 0;
     uint64_t unb_g = 0, tf_g = 0, tf2_g = 0, au_fu_tf2_pops = 0, au_fu_tf2_g = 0, viol2 = 0, au_runs = 0, au_fu_runs = 0, au_fu_tf_runs = 0;
-    uint64_t hist_exec[8] = {0}, fz_not_tf = 0, fz_not_tf_runs = 0, b0_checked_not_tf = 0, ex_cls[4] = {0, 0, 0, 0}, ex_runs_cls[4] = {0, 0, 0, 0}, ops_ref = 0, ops_exec = 0, runs_exec = 0, pops_exec = 0, fz_g = 0, fz_pops_saved = 0, fz_runs_saved = 0, fz_viol = 0, fz_det = 0, run0_unb_pops = 0, cls[4] = {0, 0, 0, 0}, cls_pops[4] = {0, 0, 0, 0}, det_tf2_pops = 0, det_tf2_g = 0;
+    uint64_t lp_g = 0, lp_exec = 0, lp_all = 0, lp_long = 0, hist_exec[8] = {0}, fz_not_tf = 0, fz_not_tf_runs = 0, b0_checked_not_tf = 0, ex_cls[4] = {0, 0, 0, 0}, ex_runs_cls[4] = {0, 0, 0, 0}, ops_ref = 0, ops_exec = 0, runs_exec = 0, pops_exec = 0, fz_g = 0, fz_pops_saved = 0, fz_runs_saved = 0, fz_viol = 0, fz_det = 0, run0_unb_pops = 0, cls[4] = {0, 0, 0, 0}, cls_pops[4] = {0, 0, 0, 0}, det_tf2_pops = 0, det_tf2_g = 0;
 #pragma omp parallel reduction(+ : tot_pops, tot_runs, om_g, om_pops, om_runs, au_pops, au_fu_pops, au_fu_tf_pops, \
                                au_tr_pops, au_fu_g, au_fu_tf_g, unb_g, tf_g, au_runs, au_fu_runs, au_fu_tf_runs, \
-                               hist_exec[:8], fz_not_tf, fz_not_tf_runs, b0_checked_not_tf, ex_cls[:4], ex_runs_cls[:4], ops_ref, ops_exec, runs_exec, pops_exec, fz_g, fz_pops_saved, fz_runs_saved, fz_viol, fz_det, run0_unb_pops, cls[:4], cls_pops[:4], det_tf2_pops, det_tf2_g, tf2_g, au_fu_tf2_pops, au_fu_tf2_g, viol2)
+                               lp_g, lp_exec, lp_all, lp_long, hist_exec[:8], fz_not_tf, fz_not_tf_runs, b0_checked_not_tf, ex_cls[:4], ex_runs_cls[:4], ops_ref, ops_exec, runs_exec, pops_exec, fz_g, fz_pops_saved, fz_runs_saved, fz_viol, fz_det, run0_unb_pops, cls[:4], cls_pops[:4], det_tf2_pops, det_tf2_g, tf2_g, au_fu_tf2_pops, au_fu_tf2_g, viol2)
     {
         orc_scratch S;
         orc_scratch_alloc(&S, d);
@@ -248,6 +248,19 @@ int main(int argc, char **argv) {
                     int b = 0;
                     while (b < 7 && ep >= (64ULL << b)) b++;
                     hist_exec[b]++;
+                    int line = 0;
+                    for (int t = 0; t < a; t++)
+                        line |= orc_bonds(E[t * 16 + 0], E[t * 16 + 2]) || orc_bonds(E[t * 16 + 1], E[t * 16 + 3]);
+                    if (line && !tf2e && !om) {
+                        lp_g++; lp_exec += ep; lp_long += ep >= 1024;
+                        /* every run of the genome executed to its end (run-parallel: no TRIVIAL exit) */
+                        for (int r = 0; r < nr; r++) lp_all += RC[r].pops;
+                        if (nr < kmax) {  /* the runs after the TRIVIAL one: estimate by the mean run */
+                            uint64_t m = 0;
+                            for (int r = 0; r < nr; r++) m += RC[r].pops;
+                            lp_all += (m / nr) * (uint64_t)(kmax - nr);
+                        }
+                    }
                 }
                 ops_exec += om ? 16 : 64;
             }
@@ -312,6 +325,8 @@ int main(int argc, char **argv) {
            (unsigned long long)hist_exec[0], (unsigned long long)hist_exec[1], (unsigned long long)hist_exec[2],
            (unsigned long long)hist_exec[3], (unsigned long long)hist_exec[4], (unsigned long long)hist_exec[5],
            (unsigned long long)hist_exec[6], (unsigned long long)hist_exec[7]);
+    printf(" \"line_prone_not_tfree\": {\"genomes\": %llu, \"executed_pops\": %llu, \"pops_if_all_runs\": %llu, \"genomes_ge_1024_pops\": %llu},\n",
+           (unsigned long long)lp_g, (unsigned long long)lp_exec, (unsigned long long)lp_all, (unsigned long long)lp_long);
     printf(" \"executed_pops_by_class\": [%llu, %llu, %llu, %llu], \"executed_runs_by_class\": [%llu, %llu, %llu, %llu],\n",
            (unsigned long long)ex_cls[0], (unsigned long long)ex_cls[1], (unsigned long long)ex_cls[2], (unsigned long long)ex_cls[3],
            (unsigned long long)ex_runs_cls[0], (unsigned long long)ex_runs_cls[1], (unsigned long long)ex_runs_cls[2], (unsigned long long)ex_runs_cls[3]);
