@@ -172,7 +172,15 @@ template <int A, bool S> const void *fast_kernel_fn_m(int mode) {
     default: return (const void *)k_classify_fast<A, S, FM_ROWS>;
   }
 }
-const void *fast_kernel_fn(int a, bool strict, int mode) {
+const void *fast_kernel_fn(int a, bool strict, int mode, int d) {
+  // d = 19 (the reference's grid, _k:8) with compile-time board geometry for the throughput modes
+  if (d == 19 && a >= 2 && (mode == FM_HIST || mode == FM_FIT)) {
+    if (mode == FM_HIST)
+      return strict ? (a == 2 ? (const void *)k_classify_fast<2, true, FM_HIST, 19> : (const void *)k_classify_fast<3, true, FM_HIST, 19>)
+                    : (a == 2 ? (const void *)k_classify_fast<2, false, FM_HIST, 19> : (const void *)k_classify_fast<3, false, FM_HIST, 19>);
+    return strict ? (a == 2 ? (const void *)k_classify_fast<2, true, FM_FIT, 19> : (const void *)k_classify_fast<3, true, FM_FIT, 19>)
+                  : (a == 2 ? (const void *)k_classify_fast<2, false, FM_FIT, 19> : (const void *)k_classify_fast<3, false, FM_FIT, 19>);
+  }
   if (strict) return a == 1 ? fast_kernel_fn_m<1, true>(mode) : a == 2 ? fast_kernel_fn_m<2, true>(mode)
                                                                      : fast_kernel_fn_m<3, true>(mode);
   return a == 1 ? fast_kernel_fn_m<1, false>(mode) : a == 2 ? fast_kernel_fn_m<2, false>(mode)
@@ -228,7 +236,8 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
     }
     if (smem <= (size_t)maxsmem) {
       const int mode = P.hist_mode ? FM_HIST : P.pay_mode ? FM_PAY : P.fit_mode ? FM_FIT : FM_ROWS;
-      const void *fn = fast_kernel_fn(P.a, P.strict != 0, mode);
+      const char *ed = getenv("TV_GENERIC_D");  // A/B: 1 = run-time d even for d = 19
+      const void *fn = fast_kernel_fn(P.a, P.strict != 0, mode, (ed && atoi(ed)) ? 0 : d);
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       int per_sm = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem));

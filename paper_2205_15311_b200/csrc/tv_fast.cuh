@@ -325,17 +325,20 @@ template <int A> constexpr int fast_threads() { return A == 3 ? TV_FAST_MAXT3 : 
 // 1 classify_batch rows, 2 GA fitness, 3 representative payloads (HIST / fit_mode / pay_mode)
 enum { FM_HIST = 0, FM_ROWS = 1, FM_FIT = 2, FM_PAY = 3 };
 
-template <int A, bool STRICT, int MODE>
+// D > 0: the grid dimension as a compile-time constant (board geometry folds into immediates);
+// D = 0: P.d at run time.
+template <int A, bool STRICT, int MODE, int D = 0>
 __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fast(const __grid_constant__ ClassifyParams P) {
   constexpr int NC = 4 * A;
+  const int GW = D ? fast_board_words(A, D) : P.GW;
   constexpr bool HIST = MODE == FM_HIST, FIT = MODE == FM_FIT, PAY = MODE == FM_PAY;
   extern __shared__ uint32_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
-  const int words_per_warp = (P.GW + P.S / 2) * 32;
+  const int words_per_warp = (GW + P.S / 2) * 32;
   FastLane Ln;
   Ln.gw = smem + warp * words_per_warp + lane;
-  Ln.sw = reinterpret_cast<uint16_t *>(smem + warp * words_per_warp + P.GW * 32) + lane;
+  Ln.sw = reinterpret_cast<uint16_t *>(smem + warp * words_per_warp + GW * 32) + lane;
   Ln.S = P.S;
   const int64_t gwarp = (int64_t)blockIdx.x * nwarps + warp;
   Ln.spill = P.spill + gwarp * (int64_t)P.spill_cap * 32 + lane;
@@ -357,14 +360,14 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
     }
     for (int s = threadIdx.x; s < P.q * 5; s += blockDim.x) c_tal[s] = 0;
   }
-  for (int w = 0; w < P.GW; w++) Ln.gw[w * 32] = 0xFFFFFFFFu;
+  for (int w = 0; w < GW; w++) Ln.gw[w * 32] = 0xFFFFFFFFu;
   __syncthreads();
 
   // board row stride RS nibbles, cell (r, c) = nibble lin = r RS + c.  a <= 2: rows of RW whole
   // words (RS = 8 RW >= d + 2), so the N and S neighbours sit RW words above / below in the same
   // nibble position; a = 3: RS = d + 2 (dense; its service passes scan and clear fewer words)
   constexpr bool ROWS = fast_rows<A>();
-  const int d = P.d, dd = d * d, RW = (d + 2 + 7) >> 3, RS = ROWS ? 8 * RW : d + 2;
+  const int d = D ? D : P.d, dd = d * d, RW = (d + 2 + 7) >> 3, RS = ROWS ? 8 * RW : d + 2;
   const uint32_t magic = (uint32_t)(0x100000000ULL / (uint64_t)RS) + 1u;
   const int cr = (d >> 1) + 1, centre = cr * RS + cr;
   const int thresh = P.service_thresh > 0 ? P.service_thresh : 16;
