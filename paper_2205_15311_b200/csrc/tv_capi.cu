@@ -226,7 +226,12 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
       while (P.S > 8 && 2 * (fast_smem_bytes(threads, P.GW, P.S, P.cta_slots, P.q) + 1024) > 228 * 1024) P.S -= 2;
     }
     P.S = std::max(4, std::min(P.S, (dd + 1) & ~1));
-    P.spill_cap = std::max(0, dd - P.S);
+    if (P.a <= 2) {  // the movelist ring (FastLane<true>::pop/push) has a power-of-two number of slots
+      int r = 4;
+      while (2 * r <= P.S) r *= 2;
+      P.S = r;
+    }
+    P.spill_cap = dd;  // spilled entries live at their own stack index
     size_t smem = fast_smem_bytes(threads, P.GW, P.S, P.cta_slots, P.q);
     int maxsmem = 0;
     CK(cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));

@@ -56,11 +56,11 @@ __device__ __forceinline__ int ffs_m(uint64_t x) {  // candidate flags never rea
   return lo ? __ffs(lo) - 1 : 31 + __ffs(hi);
 }
 
-struct FastLane {
+template <bool RING> struct FastLane {
   uint32_t *gw;     // &board word 0 of this lane (stride 32 words)
-  uint16_t *sw;     // &stack entry 0 of this lane: entry j at sw[j * 32] (lanes 2k, 2k+1 share a bank word)
+  uint16_t *sw;     // &movelist slot 0 of this lane: slot k at sw[k * 32] (lanes 2k, 2k+1 share a bank word)
   uint16_t *spill;  // &spill entry 0 of this lane (stride 32)
-  int S;
+  int mask;         // RING: ring slots - 1 (a power of two); else the shared slots S (linear stack)
   __device__ __forceinline__ uint32_t nib(int lin) const {
     return (gw[(lin >> 3) * 32] >> ((lin & 7) * 4)) & 15u;
   }
@@ -69,13 +69,40 @@ struct FastLane {
     const int s = (lin & 7) * 4;
     *p = (*p & ~(15u << s)) | (v << s);
   }
-  __device__ __forceinline__ uint32_t st_read(int j) const {
-    if (j < S) return sw[j * 32];
-    return spill[(int64_t)(j - S) * 32];
+  // Movelist as a window over a deeper stack: entries lo .. sp-1 (the top, where every push and
+  // pop happens) in a shared-memory ring of mask+1 slots, entries 0 .. lo-1 in the global spill.
+  // A push that overflows the ring evicts its bottom entry (a store, off the critical path); a pop
+  // that leaves fewer than two ring entries above spilled ones refills up to four of them (loads
+  // issued a pop ahead of their use).  So pops never wait on the spill, however deep the stack.
+  // (a = 3 keeps a linear stack: its dense board leaves ~54 shared slots, deeper stacks are rare)
+  __device__ __forceinline__ uint32_t pop(int &sp, int &lo) const {
+    if (!RING) {
+      --sp;
+      return sp < mask ? sw[sp * 32] : spill[(int64_t)sp * 32];
+    }
+    const uint32_t e = sw[((--sp) & mask) * 32];
+    if (sp - lo < 2 && lo > 0) {
+      const int n = min(lo, 4);
+      for (int i = 0; i < n; i++) {
+        --lo;
+        sw[(lo & mask) * 32] = spill[(int64_t)lo * 32];
+      }
+    }
+    return e;
   }
-  __device__ __forceinline__ void st_write(int j, uint32_t e) const {
-    if (j < S) sw[j * 32] = (uint16_t)e;
-    else spill[(int64_t)(j - S) * 32] = (uint16_t)e;
+  __device__ __forceinline__ void push(int &sp, int &lo, uint32_t e) const {
+    if (!RING) {
+      if (sp < mask) sw[sp * 32] = (uint16_t)e;
+      else spill[(int64_t)sp * 32] = (uint16_t)e;
+      ++sp;
+      return;
+    }
+    if (sp - lo > mask) {  // ring full: the bottom entry moves to the spill
+      spill[(int64_t)lo * 32] = sw[(lo & mask) * 32];
+      ++lo;
+    }
+    sw[(sp & mask) * 32] = (uint16_t)e;
+    ++sp;
   }
 };
 
@@ -336,10 +363,10 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
   const int words_per_warp = (GW + P.S / 2) * 32;
-  FastLane Ln;
+  FastLane<A <= 2> Ln;
   Ln.gw = smem + warp * words_per_warp + lane;
   Ln.sw = reinterpret_cast<uint16_t *>(smem + warp * words_per_warp + GW * 32) + lane;
-  Ln.S = P.S;
+  Ln.mask = A <= 2 ? P.S - 1 : P.S;  // a <= 2: the host sizes the ring as a power of two
   const int64_t gwarp = (int64_t)blockIdx.x * nwarps + warp;
   Ln.spill = P.spill + gwarp * (int64_t)P.spill_cap * 32 + lane;
   uint32_t *rh = P.run_hash + gwarp * (int64_t)P.kmax * 32 + lane;  // run r at rh[r*32]
@@ -376,7 +403,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
   int st = ST_NEED, pend = -1;
   int64_t item = 0;
   uint64_t idx = 0, rs = 0;
-  int run = 0, replay = 0, sp = 0;
+  int run = 0, replay = 0, sp = 0, lo = 0;  // movelist: sp entries, the lowest lo of them spilled
   int minr = 0, maxr = 0, minc = 0, maxc = 0;
   int trivial_at = -1, first_unbound = -1, first_mismatch = -1;
   uint32_t hash0 = 0, best = 0, fit0 = 0;
@@ -638,10 +665,11 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
           const uint32_t dir = (nbp >> (8 * j)) & 3u;
           const int dl = (dir & 1u) ? 1 : RS;
           const int nl = ((dir + 1u) & 2u) ? centre + dl : centre - dl;
-          Ln.st_write(j, (uint32_t)nl);
+          Ln.sw[j * 32] = (uint16_t)nl;  // ring slots 0..3 (the ring has >= 4 slots)
           Ln.set_nib(nl, 0xEu);
         }
         sp = 4;
+        lo = 0;
       }
       nlive = __popc(__ballot_sync(0xFFFFFFFFu, st != ST_DONE));
       if (nlive == 0) break;
@@ -650,7 +678,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
     if (st != ST_RUN || pend >= 0) continue;
 
     // =================== one movelist pop (_k:138-248) ===================
-    const int lin = (int)Ln.st_read(--sp);
+    const int lin = (int)Ln.pop(sp, lo);
     uint32_t *const pw = Ln.gw + (lin >> 3) * 32;  // the popped cell's word
     const int sh = (lin & 7) * 4;
     // neighbour values times 4 (0x3C = empty), each one rotate of its word: nibble at bit p
@@ -708,11 +736,10 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
     for (int j = 0; j < 3; j++) {
       if (j < mm) {
         const int nl = lin + (int)((nbp >> (8 * j)) & 0xFFu) - 128;
-        Ln.st_write(sp + j, (uint32_t)nl);
+        Ln.push(sp, lo, (uint32_t)nl);
         atomicAnd(&Ln.gw[(nl >> 3) * 32], ~(1u << ((nl & 7) * 4)));  // F -> E (one ATOMS, lane-private word)
       }
     }
-    sp += mm;
     if (mm < m) pend = RUN_OVERFLOW;
     else if (sp == 0) pend = RUN_BOUNDED;
   }
