@@ -268,7 +268,7 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
       // 1-mers (seed faces bond nothing) classified by the pre-pass and sorted past the end of
       // the fast kernel's work (k_prepass).  TV_ONEMER=0 disables it.
       const char *e1 = getenv("TV_ONEMER");
-      const bool want_onemer = want_order && !P.fit_mode && (e1 ? atoi(e1) != 0 : true);
+      const bool want_onemer = want_order && (e1 ? atoi(e1) != 0 : true);
       // histogram mode runs in slices of <= 2^26 items (sort and flag scratch stay bounded;
       // the histogram accumulates across slices)
       const int64_t n_all = P.n, slice = P.hist_mode ? ((int64_t)1 << 26) : n_all;

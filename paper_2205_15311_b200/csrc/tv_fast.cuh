@@ -847,7 +847,11 @@ __global__ void __launch_bounds__(256, TV_PREPASS_MINB) k_prepass(const __grid_c
         kk = (kk << 1) | (f ? 0u : 1u);  // trivial-freedom as the lowest key bit
         key_out[item] = om ? kOneMerKey : (uint16_t)kk;
         iota_out[item] = (uint32_t)item | (f ? 0x80000000u : 0u);  // items < 2^31; bit 31 = flag
-        if (om && !P.hist_mode) {  // classify_batch row of a DET 1x1 genome (_k:438-452)
+        if (om && P.fit_mode) {  // GA fitness of a DET 1x1 genome: d^2 - shapediff(target, centre cell)
+          const int cr = (P.d >> 1) + 1;
+          const int ov = (int)((P.target_rows[cr] >> cr) & 1u);
+          P.out_fit[item] = (uint32_t)(P.d * P.d - (P.target_cells + 1 - 2 * ov));
+        } else if (om && !P.hist_mode) {  // classify_batch row of a DET 1x1 genome (_k:438-452)
           for (int k = 0; k < P.q; k++) P.out_class[item * P.q + k] = (uint8_t)CLS_DET;
           P.out_hash[item] = kOneMerHash;
           P.out_w[item] = 1; P.out_h[item] = 1; P.out_cells[item] = 1;
