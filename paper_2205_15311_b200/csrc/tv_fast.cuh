@@ -344,7 +344,7 @@ __host__ __device__ inline int fast_board_words(int a, int d) {
 #define TV_FAST_MAXT 384  // 2 x 384 lanes per SM: 24 warps at <= 80 registers (measured +10% vs 2 x 256)
 #endif
 #ifndef TV_FAST_MAXT3
-#define TV_FAST_MAXT3 320  // a = 3: 64-bit candidate planes need 96 registers (S32 block 34.7 -> 33.7 ms)
+#define TV_FAST_MAXT3 352  // a = 3: 2 x 352 lanes at <= 80 registers (round 2: S32 block 22.07 -> 21.44 ms vs 2 x 320 at 96)
 #endif
 template <int A> constexpr int fast_threads() { return A == 3 ? TV_FAST_MAXT3 : TV_FAST_MAXT; }
 
