@@ -677,8 +677,9 @@ def main():
             pass
         roof = enum_roofline("k_classify_fast<2>", N_S28 / world, kms, peak, event_counts("s28_full"),
                              "one tv_enumerate_chunks call: k_prepass<2> (trivial-freedom proof, 1-mers, behaviour "
-                             "key, ~1.4 ms) + CUB radix sort of the keys (~0.2 ms) + k_classify_fast<2> "
-                             "(conservative: all three kernels' time)", traffic)
+                             "key + tile key histograms, ~1.3 ms) + the counting sort by key (k_key_binscan / "
+                             "basescan / scatter, ~0.17 ms) + k_classify_fast<2> (conservative: all five kernels' "
+                             "time)", traffic)
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         try:
@@ -704,9 +705,10 @@ def main():
                 "e2e": {"value": N_S28 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                         "d2h_bytes_per_step": int(d2h), "api": "classify.enumerate_space"},
                 "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(),
-                # ours per step: k_hist_reset, k_prepass, k_classify_fast (+ at N > 1 the exchange:
-                # k_hist_compact, k_hist_pack, k_hist_reset, k_hist_merge, k_hist_merge_rows1/2)
-                "gpu_launches": (3 if world == 1 else 9) * args.steps, "s32": s32, "ga": ga, "ga_jatam": ga_jatam,
+                # ours per step: k_hist_reset, k_prepass, k_key_binscan, k_key_basescan, k_key_scatter,
+                # k_classify_fast (+ at N > 1 the exchange: k_hist_compact, k_hist_pack, k_hist_reset,
+                # k_hist_merge, k_hist_merge_rows1/2); no library kernel on the step
+                "gpu_launches": (6 if world == 1 else 12) * args.steps, "s32": s32, "ga": ga, "ga_jatam": ga_jatam,
                 "ga_sweep": ga_sweep, "mutation_L1024": mutation}
         print(json.dumps(line), flush=True)
     hist.close()

@@ -273,19 +273,15 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
       // the histogram accumulates across slices)
       const int64_t n_all = P.n, slice = P.hist_mode ? ((int64_t)1 << 26) : n_all;
       const int64_t smax = std::min(n_all, slice);
-      uint32_t *flags = nullptr, *order = nullptr, *iota = nullptr;
-      uint16_t *key = nullptr, *key_sorted = nullptr;
+      uint32_t *flags = nullptr, *order = nullptr, *iota = nullptr, *tile_hist = nullptr, *bintot = nullptr;
+      uint16_t *key = nullptr;
       unsigned long long *n_skip = nullptr;
       if (want_onemer) CK(S.get(&n_skip, 1));
-      uint8_t *tmp = nullptr;
-      size_t tmp_bytes = 0;
-      const int64_t nwmax = (smax + 31) / 32;
+      const int64_t nwmax = (smax + 31) / 32, ntmax = (smax + kKeyTile - 1) / kKeyTile;
       if (want_flags) CK(S.get(&flags, (size_t)nwmax));
-      if (want_order) {
-        CK(S.get(&order, (size_t)smax)); CK(S.get(&iota, (size_t)smax));
-        CK(S.get(&key, (size_t)smax)); CK(S.get(&key_sorted, (size_t)smax));
-        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key, key_sorted, iota, order, (int)smax, 0, TV_KEY_BITS, st));
-        CK(S.get(&tmp, tmp_bytes));
+      if (want_order) {  // counting sort by key (k_prepass tile histograms + k_key_*), no library sort
+        CK(S.get(&order, (size_t)smax)); CK(S.get(&iota, (size_t)smax)); CK(S.get(&key, (size_t)smax));
+        CK(S.get(&tile_hist, (size_t)kNumKeys * ntmax)); CK(S.get(&bintot, (size_t)kNumKeys));
       }
       const void *ff = P.strict
           ? (P.a == 1 ? (const void *)k_prepass<1, true>
@@ -301,15 +297,17 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
         if (off > 0) CK(cudaMemsetAsync(work, 0, sizeof(unsigned long long), st));
         if (n_skip) CK(cudaMemsetAsync(n_skip, 0, sizeof(unsigned long long), st));
         if (want_flags || want_order) {
-          const int64_t nw = (P.n + 31) / 32;
-          const int64_t fb = std::min<int64_t>((nw * 32 + 255) / 256, (int64_t)nsm * 8);
+          int64_t ntiles = (P.n + kKeyTile - 1) / kKeyTile;
           uint16_t *kk = want_order ? key : nullptr;
           uint32_t *ff_flags = want_flags ? flags : nullptr;
-          void *fargs[] = {&P, &ff_flags, &kk, &iota, &n_skip};
-          CK(cudaLaunchKernel(ff, dim3((unsigned)fb), dim3(256), fargs, 0, st));
-          if (want_order) {  // stable LSD radix sort of the items by their 10-bit behaviour key
-            size_t tb = tmp_bytes;
-            CK(cub::DeviceRadixSort::SortPairs(tmp, tb, key, key_sorted, iota, order, (int)P.n, 0, TV_KEY_BITS, st));
+          uint32_t *th = want_order ? tile_hist : nullptr;
+          void *fargs[] = {&P, &ff_flags, &kk, &iota, &n_skip, &th, &ntiles};
+          CK(cudaLaunchKernel(ff, dim3((unsigned)ntiles), dim3(256), fargs, 0, st));
+          if (want_order) {  // counting sort of the items by their behaviour key
+            k_key_binscan<<<kNumKeys, 1024, 0, st>>>(tile_hist, ntiles, bintot);
+            k_key_basescan<<<1, 1024, 0, st>>>(bintot);
+            k_key_scatter<<<(unsigned)ntiles, 256, 0, st>>>(key, iota, tile_hist, ntiles, bintot, P.n, order);
+            CK(cudaGetLastError());
           }
           P.tf_flags = ff_flags;
           P.order = want_order ? order : nullptr;

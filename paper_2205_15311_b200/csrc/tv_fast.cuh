@@ -784,23 +784,32 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
 constexpr uint32_t kOneMerHash = 0x3a9be4cfu;  // OAT of (w, h, x, y) = (1, 1, 0, 0), _k:260-277
 constexpr uint16_t kOneMerKey = (1u << TV_KEY_BITS) - 1u;
 
+//  * work order (with key): the items are counting-sorted by key (k_key_binscan / _basescan /
+//    _scatter below, no library sort): CTA b handles the tile of items [b TILE, (b+1) TILE) and
+//    writes the tile's key histogram to tile_hist[key * ntiles + b].
+constexpr int kNumKeys = 1 << TV_KEY_BITS;
+constexpr int kKeyTile = 16384;  // items per pre-pass / scatter CTA (multiple of 32)
+
 template <int A, bool STRICT>
 __global__ void __launch_bounds__(256, TV_PREPASS_MINB) k_prepass(const __grid_constant__ ClassifyParams P, uint32_t *flags,
                                                  uint16_t *key_out, uint32_t *iota_out,
-                                                 unsigned long long *n_skip) {
+                                                 unsigned long long *n_skip, uint32_t *tile_hist, int64_t ntiles) {
   constexpr int NC = 4 * A;
-  const int64_t nw = (P.n + 31) >> 5;
   const int lane = threadIdx.x & 31;
   __shared__ unsigned long long s_om_min;
   __shared__ unsigned int s_om_cnt;
+  __shared__ uint32_t s_hist[kNumKeys];
   if (threadIdx.x == 0) { s_om_min = ~0ULL; s_om_cnt = 0u; }
+  if (tile_hist)
+    for (int b = threadIdx.x; b < kNumKeys; b += blockDim.x) s_hist[b] = 0u;
   __syncthreads();
-  for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~(int64_t)31; base < nw * 32;
-       base += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t t0 = (int64_t)blockIdx.x * kKeyTile, t1 = min(P.n, t0 + kKeyTile);
+  for (int64_t base = t0 + (threadIdx.x & ~31); base < t1; base += blockDim.x) {
     const int64_t item = base + lane;
     bool f = false, om = false;
-    const bool valid = item < P.n;
+    const bool valid = item < t1;
     uint64_t idx = 0;
+    uint32_t kk_all = 0xFFFFFFFFu;  // this item's key for the tile histogram (none if invalid)
     if (valid) {
       idx = item_index(P.indices, P.start, P.chunk, P.stride, P.item0 + item);
       uint32_t lab[12];
@@ -845,7 +854,9 @@ __global__ void __launch_bounds__(256, TV_PREPASS_MINB) k_prepass(const __grid_c
       }
       if (key_out) {
         kk = (kk << 1) | (f ? 0u : 1u);  // trivial-freedom as the lowest key bit
-        key_out[item] = om ? kOneMerKey : (uint16_t)kk;
+        kk = om ? kOneMerKey : kk;
+        key_out[item] = (uint16_t)kk;
+        kk_all = kk;
         iota_out[item] = (uint32_t)item | (f ? 0x80000000u : 0u);  // items < 2^31; bit 31 = flag
         if (om && P.fit_mode) {  // GA fitness of a DET 1x1 genome: d^2 - shapediff(target, centre cell)
           const int cr = (P.d >> 1) + 1;
@@ -863,6 +874,10 @@ __global__ void __launch_bounds__(256, TV_PREPASS_MINB) k_prepass(const __grid_c
       const uint32_t w = __ballot_sync(0xFFFFFFFFu, f);
       if (lane == 0) flags[base >> 5] = w;
     }
+    if (tile_hist) {  // warp-aggregated count per key
+      const unsigned peers = __match_any_sync(0xFFFFFFFFu, kk_all);
+      if (kk_all != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&s_hist[kk_all], (uint32_t)__popc(peers));
+    }
     if (n_skip) {
       const unsigned om_mask = __ballot_sync(0xFFFFFFFFu, om);
       if (om_mask) {
@@ -875,6 +890,10 @@ __global__ void __launch_bounds__(256, TV_PREPASS_MINB) k_prepass(const __grid_c
         if (lane == 0) { atomicAdd(&s_om_cnt, (unsigned)__popc(om_mask)); atomicMin(&s_om_min, m); }
       }
     }
+  }
+  if (tile_hist) {
+    __syncthreads();
+    for (int b = threadIdx.x; b < kNumKeys; b += blockDim.x) tile_hist[(int64_t)b * ntiles + blockIdx.x] = s_hist[b];
   }
   if (n_skip) {
     __syncthreads();
@@ -896,6 +915,109 @@ __global__ void __launch_bounds__(256, TV_PREPASS_MINB) k_prepass(const __grid_c
         }
       }
     }
+  }
+}
+
+// Counting sort of the work items by key (replaces a library radix sort on the hot step).
+// tile_hist is key-major [key][tile]; after k_key_binscan it holds each (key, tile)'s offset
+// inside its key's run and bintot[key] the key's total; k_key_basescan turns bintot into the
+// key runs' starts; k_key_scatter places every item (warp-aggregated shared cursor per key).
+// Within one key the order follows the tiles and, inside a tile, the warps' arrival -- results
+// never depend on the order (per-genome substreams, commutative histogram updates).
+__global__ void __launch_bounds__(1024) k_key_binscan(uint32_t *tile_hist, int64_t ntiles, uint32_t *bintot) {
+  __shared__ uint32_t ws[32];
+  __shared__ uint32_t carry;
+  uint32_t *row = tile_hist + (int64_t)blockIdx.x * ntiles;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwp = blockDim.x >> 5;
+  if (threadIdx.x == 0) carry = 0u;
+  __syncthreads();
+  for (int64_t t0 = 0; t0 < ntiles; t0 += blockDim.x) {
+    const int64_t t = t0 + threadIdx.x;
+    const uint32_t v = t < ntiles ? row[t] : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      const uint32_t w0 = lane < nwp ? ws[lane] : 0u;
+      uint32_t w = w0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, w, o);
+        if (lane >= o) w += y;
+      }
+      ws[lane] = w - w0;
+    }
+    __syncthreads();
+    const uint32_t c = carry;
+    if (t < ntiles) row[t] = c + ws[wid] + x - v;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = c + ws[wid] + x;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) bintot[blockIdx.x] = carry;
+}
+
+// exclusive scan of the kNumKeys key totals in place (kNumKeys a multiple of 1024)
+__global__ void __launch_bounds__(1024) k_key_basescan(uint32_t *bintot) {
+  __shared__ uint32_t ws[32];
+  __shared__ uint32_t carry;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0u;
+  __syncthreads();
+  for (int b0 = 0; b0 < kNumKeys; b0 += 1024) {
+    const int b = b0 + threadIdx.x;
+    const uint32_t v = bintot[b];
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      const uint32_t w0 = ws[lane];
+      uint32_t w = w0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, w, o);
+        if (lane >= o) w += y;
+      }
+      ws[lane] = w - w0;
+    }
+    __syncthreads();
+    const uint32_t c = carry;
+    bintot[b] = c + ws[wid] + x - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = c + ws[wid] + x;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_key_scatter(const uint16_t *key, const uint32_t *iota,
+                                                     const uint32_t *tile_hist, int64_t ntiles,
+                                                     const uint32_t *binbase, int64_t n, uint32_t *order) {
+  __shared__ uint32_t cur[kNumKeys];
+  for (int b = threadIdx.x; b < kNumKeys; b += blockDim.x)
+    cur[b] = binbase[b] + tile_hist[(int64_t)b * ntiles + blockIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t t0 = (int64_t)blockIdx.x * kKeyTile, t1 = min(n, t0 + kKeyTile);
+  for (int64_t base = t0 + (threadIdx.x & ~31); base < t1; base += blockDim.x) {
+    const int64_t item = base + lane;
+    const bool valid = item < t1;
+    const uint32_t k = valid ? key[item] : 0xFFFFFFFFu;
+    const unsigned peers = __match_any_sync(0xFFFFFFFFu, k);
+    const int leader = __ffs(peers) - 1;
+    uint32_t pos = 0;
+    if (valid && lane == leader) pos = atomicAdd(&cur[k], (uint32_t)__popc(peers));
+    pos = __shfl_sync(0xFFFFFFFFu, pos, leader) + (uint32_t)__popc(peers & ((1u << lane) - 1u));
+    if (valid) order[pos] = iota[item];
   }
 }
 
