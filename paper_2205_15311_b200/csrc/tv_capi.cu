@@ -1068,6 +1068,7 @@ struct tv_ga {
   unsigned long long *donew;
   void *scan_tmp;
   size_t scan_bytes;
+  void *arena;  // narrow GA: one allocation holding P's buffers
 };
 
 int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **out) {
@@ -1120,15 +1121,27 @@ int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **
   h->device = dev;
   h->cur = 0;
   cudaError_t e = cudaSuccess;
-  e = e ? e : cudaMalloc(&P.pop0, n * 8);
-  e = e ? e : cudaMalloc(&P.pop1, n * 8);
-  e = e ? e : cudaMalloc(&P.cdf, n * 4);
-  e = e ? e : cudaMalloc(&P.guide, (size_t)n * sizeof(ulonglong2));
-  e = e ? e : cudaMalloc(&P.fstage, n * 4);
-  e = e ? e : cudaMalloc(&P.tot, (size_t)h->nblocks * 8);
-  e = e ? e : cudaMalloc(&P.rowx, (size_t)h->nblocks * (size_t)(P.chunk / 32) * 4);
-  e = e ? e : cudaMalloc(&P.done, 8);
-  e = e ? e : cudaMalloc(&P.final_buf, 4);
+  {  // one arena for the generation loop's buffers
+    const size_t al = 4096;
+    const size_t sz[9] = {(size_t)n * 8, (size_t)n * 8, (size_t)n * 4, (size_t)n * sizeof(ulonglong2), (size_t)n * 4,
+                          (size_t)h->nblocks * 8, (size_t)h->nblocks * (size_t)(P.chunk / 32) * 4, 8, 4};
+    size_t off[9], total = 0;
+    for (int i = 0; i < 9; i++) { off[i] = total; total += (sz[i] + al - 1) / al * al; }
+    char *base = nullptr;
+    e = cudaMalloc(&base, total);
+    if (e == cudaSuccess) {
+      h->arena = base;
+      P.pop0 = reinterpret_cast<unsigned long long *>(base + off[0]);
+      P.pop1 = reinterpret_cast<unsigned long long *>(base + off[1]);
+      P.cdf = reinterpret_cast<uint32_t *>(base + off[2]);
+      P.guide = reinterpret_cast<ulonglong2 *>(base + off[3]);
+      P.fstage = reinterpret_cast<uint32_t *>(base + off[4]);
+      P.tot = reinterpret_cast<unsigned long long *>(base + off[5]);
+      P.rowx = reinterpret_cast<uint32_t *>(base + off[6]);
+      P.done = reinterpret_cast<unsigned long long *>(base + off[7]);
+      P.final_buf = reinterpret_cast<int32_t *>(base + off[8]);
+    }
+  }
   e = e ? e : cudaMemset(P.pop0, 0, n * 8);
   if (e != cudaSuccess) { tv_ga_destroy(h); return fail(TV_ERR_CUDA, "GA allocation: %s", cudaGetErrorString(e)); }
   *out = h;
@@ -1138,9 +1151,13 @@ int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **
 int tv_ga_destroy(tv_ga *h) {
   if (!h) return 0;
   GaParams &P = h->P;
-  cudaFree(P.pop0); cudaFree(P.pop1); cudaFree(P.cdf); cudaFree(P.guide); cudaFree(P.fstage); cudaFree(P.tot);
-  cudaFree(P.rowx);
-  cudaFree(P.done); cudaFree(P.final_buf);
+  if (h->arena) {
+    cudaFree(h->arena);
+  } else {
+    cudaFree(P.pop0); cudaFree(P.pop1); cudaFree(P.cdf); cudaFree(P.guide); cudaFree(P.fstage); cudaFree(P.tot);
+    cudaFree(P.rowx);
+    cudaFree(P.done); cudaFree(P.final_buf);
+  }
   cudaFree(h->Tw); cudaFree(h->fw); cudaFree(h->cdfw); cudaFree(h->flags); cudaFree(h->donew); cudaFree(h->scan_tmp);
   delete h;
   return 0;
