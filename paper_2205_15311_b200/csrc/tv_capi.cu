@@ -271,7 +271,9 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
       const bool want_onemer = want_order && (e1 ? atoi(e1) != 0 : true);
       // histogram mode runs in slices of <= 2^26 items (sort and flag scratch stay bounded;
       // the histogram accumulates across slices)
-      const int64_t n_all = P.n, slice = P.hist_mode ? ((int64_t)1 << 26) : n_all;
+      const char *esl = getenv("TV_SLICE_LOG2");  // A/B: histogram-mode slice size (items <= 2^31)
+      const int slog = esl ? std::max(16, std::min(30, atoi(esl))) : 26;
+      const int64_t n_all = P.n, slice = P.hist_mode ? ((int64_t)1 << slog) : n_all;
       const int64_t smax = std::min(n_all, slice);
       uint32_t *flags = nullptr, *order = nullptr, *iota = nullptr, *tile_hist = nullptr, *bintot = nullptr;
       uint16_t *key = nullptr;
