@@ -10,8 +10,11 @@
 //           rows, N/S neighbours at a fixed word offset; RS = d+2 for a = 3);
 //           0..4a-1 = placed candidate t*4+orient, 0xE = empty + on the
 //           movelist, 0xF = empty.
-//   stack : S u16 entries/lane (entry = lin; entry j of lane L at halfword
-//           j*32+L), spilled to global beyond S.
+//   stack : S u16 slots/lane (entry = lin; slot k of lane L at halfword k*32+L).
+//           a <= 2: a ring holding the top S entries (S a power of two), the
+//           ones below spilled to global and refilled ahead of use
+//           (FastLane<true>); a = 3: entries 0..S-1 here, deeper ones in
+//           global (FastLane<false>).
 // Per CTA: a small open-addressed phenotype cache (histogram mode) and the
 // class tallies, flushed to the global table once at the end.
 //
