@@ -1071,6 +1071,8 @@ struct tv_ga {
   void *scan_tmp;
   size_t scan_bytes;
   void *arena;  // narrow GA: one allocation holding P's buffers
+  uint32_t *fknown;   // per individual of the current population: its fitness if known (GaParams::f_known)
+  bool fknown_valid;  // fknown describes the current population
 };
 
 int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **out) {
@@ -1125,10 +1127,11 @@ int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **
   cudaError_t e = cudaSuccess;
   {  // one arena for the generation loop's buffers
     const size_t al = 4096;
-    const size_t sz[9] = {(size_t)n * 8, (size_t)n * 8, (size_t)n * 4, (size_t)n * sizeof(ulonglong2), (size_t)n * 4,
-                          (size_t)h->nblocks * 8, (size_t)h->nblocks * (size_t)(P.chunk / 32) * 4, 8, 4};
-    size_t off[9], total = 0;
-    for (int i = 0; i < 9; i++) { off[i] = total; total += (sz[i] + al - 1) / al * al; }
+    const size_t sz[10] = {(size_t)n * 8, (size_t)n * 8, (size_t)n * 4, (size_t)n * sizeof(ulonglong2), (size_t)n * 4,
+                          (size_t)h->nblocks * 8, (size_t)h->nblocks * (size_t)(P.chunk / 32) * 4, 8, 4,
+                          (size_t)n * 4};
+    size_t off[10], total = 0;
+    for (int i = 0; i < 10; i++) { off[i] = total; total += (sz[i] + al - 1) / al * al; }
     char *base = nullptr;
     e = cudaMalloc(&base, total);
     if (e == cudaSuccess) {
@@ -1142,6 +1145,7 @@ int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **
       P.rowx = reinterpret_cast<uint32_t *>(base + off[6]);
       P.done = reinterpret_cast<unsigned long long *>(base + off[7]);
       P.final_buf = reinterpret_cast<int32_t *>(base + off[8]);
+      h->fknown = reinterpret_cast<uint32_t *>(base + off[9]);
     }
   }
   e = e ? e : cudaMemset(P.pop0, 0, n * 8);
@@ -1168,6 +1172,7 @@ int tv_ga_destroy(tv_ga *h) {
 int tv_ga_set_population(tv_ga *h, const uint64_t *genomes, void *stream) {
   if (!h) return fail(TV_ERR_ARG, "null GA");
   cudaStream_t st = (cudaStream_t)stream;
+  h->fknown_valid = false;
   unsigned long long *dst = h->cur ? h->P.pop1 : h->P.pop0;
   const int64_t words = h->P.n * h->W;
   if (!genomes) {
@@ -1270,6 +1275,7 @@ int tv_ga_run(tv_ga *h, uint64_t seed, int64_t g0, int64_t n_gens, uint32_t targ
   if (h->cur) std::swap(P.pop0, P.pop1);
   P.seed = seed; P.g0 = g0; P.n_gens = n_gens; P.target = target; P.adapt_count = adapt_count;
   P.stop_when = stop_when; P.fitness = f_ext ? 1 : 0; P.f_ext = f_ext;
+  P.f_known = f_ext ? h->fknown : nullptr;  // children equal to a parent inherit its fitness (one generation)
   int64_t done = 0;
   int32_t fb = 0;
   {
@@ -1302,6 +1308,7 @@ int tv_ga_run(tv_ga *h, uint64_t seed, int64_t g0, int64_t n_gens, uint32_t targ
   }
   CK(cudaStreamSynchronize(st));
   h->cur ^= fb;
+  h->fknown_valid = f_ext && fb;  // a reproduced generation with external fitness wrote fknown
   if (gens_done) *gens_done = done;
   return 0;
 }
@@ -1413,6 +1420,8 @@ int tv_ga_fitness_jatam(tv_ga *h, int32_t a, int32_t bpl, const int64_t *mask_po
   P.target_cells = tc;
   P.indices = reinterpret_cast<const uint64_t *>(h->cur ? h->P.pop1 : h->P.pop0);
   P.n = h->P.n;
+  const char *efc = getenv("TV_FITCACHE");  // 0: classify every genome (A/B)
+  P.fit_known = (h->fknown_valid && (efc ? atoi(efc) != 0 : true)) ? h->fknown : nullptr;
   Scratch S(st);
   return launch_classify(C, S, st);
 }

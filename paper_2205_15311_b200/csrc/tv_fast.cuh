@@ -848,7 +848,10 @@ __global__ void __launch_bounds__(256, TV_PREPASS_MINB) k_prepass(const __grid_c
         }
         kk = ((line ? 0u : 1u) << 9) | ((self0 ? 0u : 1u) << 8) | ((uint32_t)(4 - nb0) << 5) |
              ((selfr ? 0u : 1u) << 4) | (uint32_t)(8 - nbr);
-        om = n_skip != nullptr && nb0 == 0;
+        // GA fitness mode: a genome whose fitness the GA generation already knows (a child equal
+        // to its parent, GaParams::f_known) is skipped like a 1-mer
+        const bool known = P.fit_mode && P.fit_known && P.fit_known[item] != 0xFFFFFFFFu;
+        om = n_skip != nullptr && (nb0 == 0 || known);
       }
       if (flags && !om) {  // (1-mers never reach the fast kernel)
         Cand<A, STRICT> K;
@@ -861,10 +864,11 @@ __global__ void __launch_bounds__(256, TV_PREPASS_MINB) k_prepass(const __grid_c
         key_out[item] = (uint16_t)kk;
         kk_all = kk;
         iota_out[item] = (uint32_t)item | (f ? 0x80000000u : 0u);  // items < 2^31; bit 31 = flag
-        if (om && P.fit_mode) {  // GA fitness of a DET 1x1 genome: d^2 - shapediff(target, centre cell)
+        if (om && P.fit_mode) {  // known fitness, or that of a DET 1x1 genome: d^2 - shapediff(target, centre)
           const int cr = (P.d >> 1) + 1;
           const int ov = (int)((P.target_rows[cr] >> cr) & 1u);
-          P.out_fit[item] = (uint32_t)(P.d * P.d - (P.target_cells + 1 - 2 * ov));
+          const uint32_t fk = P.fit_known ? P.fit_known[item] : 0xFFFFFFFFu;
+          P.out_fit[item] = fk != 0xFFFFFFFFu ? fk : (uint32_t)(P.d * P.d - (P.target_cells + 1 - 2 * ov));
         } else if (om && !P.hist_mode) {  // classify_batch row of a DET 1x1 genome (_k:438-452)
           for (int k = 0; k < P.q; k++) P.out_class[item * P.q + k] = (uint8_t)CLS_DET;
           P.out_hash[item] = kOneMerHash;

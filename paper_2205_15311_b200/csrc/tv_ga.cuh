@@ -55,6 +55,7 @@ struct GaParams {
   uint64_t T[64];        // Poisson CDF thresholds x 2^63 (k = #{j < L : (draw >> 1) >= T[j]})
   unsigned long long *pop0, *pop1;
   const uint32_t *f_ext;
+  uint32_t *f_known;     // external fitness: per child, its fitness if it equals a parent, else ~0 (or nullptr)
   uint32_t *cdf;         // n
   uint32_t *fstage;      // n: fitness staged in index order (own chunk per CTA)
   ulonglong2 *guide;     // n buckets (first B used per generation): x = (cdf[j] << 32) | j,
@@ -142,8 +143,8 @@ __device__ __forceinline__ uint32_t ga_pick(const GaParams &P, uint32_t r, uint3
 // returned: one L2 read when the bucket owner covers r, one more per step
 // (cdf and genome in the same word) otherwise.
 __device__ __forceinline__ uint64_t ga_pick_genome(const GaParams &P, const unsigned long long *pop, uint32_t r,
-                                                   uint32_t total, uint64_t mul) {
-  if (total == 0) return pop[r] & 0xFFFFFFFFull;
+                                                   uint32_t total, uint64_t mul, uint32_t &jo) {
+  if (total == 0) { jo = r; return pop[r] & 0xFFFFFFFFull; }
   const ulonglong2 e = P.guide[(uint32_t)(((uint64_t)r * mul) >> 32)];
   uint32_t j = (uint32_t)e.x, c = (uint32_t)(e.x >> 32);
   uint64_t g = e.y;
@@ -152,6 +153,7 @@ __device__ __forceinline__ uint64_t ga_pick_genome(const GaParams &P, const unsi
     c = (uint32_t)(v >> 32);
     g = v & 0xFFFFFFFFull;
   }
+  jo = j;
   return g;
 }
 
@@ -336,17 +338,19 @@ __global__ void __launch_bounds__(TV_GA_THREADS, 1) k_ga_run(const __grid_consta
         const int64_t iu = i + u * nt;
         D[u] = iu < c1 ? ga_draws(P, gkey, iu, total) : D[0];
       }
-      uint64_t cv[NI];
+      uint64_t cv[NI], ga_[NI], gb_[NI];  // child before mutation, parents' genomes
+      uint32_t pa[NI], pb[NI];              // parents' indices
       if (packed) {
 #pragma unroll
-        for (int u = 0; u < NI; u++) cv[u] = ga_pick_genome(P, pop, D[u].ra, total, mul);
+        for (int u = 0; u < NI; u++) { ga_[u] = ga_pick_genome(P, pop, D[u].ra, total, mul, pa[u]); cv[u] = ga_[u]; }
         if (P.mode != 0) {
 #pragma unroll
-          for (int u = 0; u < NI; u++)
-            cv[u] = (cv[u] & D[u].top) | (ga_pick_genome(P, pop, D[u].rb, total, mul) & ~D[u].top);
+          for (int u = 0; u < NI; u++) {
+            gb_[u] = ga_pick_genome(P, pop, D[u].rb, total, mul, pb[u]);
+            cv[u] = (cv[u] & D[u].top) | (gb_[u] & ~D[u].top);
+          }
         }
       } else {
-        uint32_t pa[NI], pb[NI];
 #pragma unroll
         for (int u = 0; u < NI; u++) pa[u] = ga_pick(P, D[u].ra, total, mul);
         if (P.mode != 0) {
@@ -354,10 +358,10 @@ __global__ void __launch_bounds__(TV_GA_THREADS, 1) k_ga_run(const __grid_consta
           for (int u = 0; u < NI; u++) pb[u] = ga_pick(P, D[u].rb, total, mul);
         }
 #pragma unroll
-        for (int u = 0; u < NI; u++) cv[u] = pop[pa[u]];
+        for (int u = 0; u < NI; u++) { ga_[u] = pop[pa[u]]; cv[u] = ga_[u]; }
         if (P.mode != 0) {
 #pragma unroll
-          for (int u = 0; u < NI; u++) cv[u] = (cv[u] & D[u].top) | (pop[pb[u]] & ~D[u].top);
+          for (int u = 0; u < NI; u++) { gb_[u] = pop[pb[u]]; cv[u] = (cv[u] & D[u].top) | (gb_[u] & ~D[u].top); }
         }
       }
 #pragma unroll
@@ -373,6 +377,12 @@ __global__ void __launch_bounds__(TV_GA_THREADS, 1) k_ga_run(const __grid_consta
             P.fstage[iu] = f;
           } else {
             f = P.fstage[iu];  // external fitness stays that of the staged population
+            if (P.f_known) {   // a child equal to a parent has that parent's (deterministic) fitness
+              uint32_t fk = 0xFFFFFFFFu;
+              if (c == (ga_[u] & full)) fk = P.fstage[pa[u]];
+              else if (P.mode != 0 && c == (gb_[u] & full)) fk = P.fstage[pb[u]];
+              P.f_known[iu] = fk;
+            }
           }
         }
         if (r < nrows) {  // warp-uniform: a warp's lanes make one row

@@ -41,6 +41,7 @@ struct ClassifyParams {
   int32_t fit_mode;
   int32_t target_cells;
   uint32_t *out_fit;
+  const uint32_t *fit_known;  // per item: fitness known from the GA generation (~0 = unknown), or nullptr
   uint32_t target_rows[32];
   // scratch
   uint32_t *run_hash;       // per lane, kmax entries

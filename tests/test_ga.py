@@ -468,3 +468,27 @@ def test_mutation_benchmark_device_equals_restatement_and_speedup():
     r = E.mutation_benchmark(pop_size=1 << 18, length=1024, mu_L=0.5, reps=3)
     assert r["speedup"] >= 2.0, r
     assert abs(r["distribution_flips_per_genome"] - 0.5) < 0.02 and abs(r["bitwise_flips_per_genome"] - 0.5) < 0.02
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", [0, 2])
+def test_jatam_fitness_cache_is_exact(mode, monkeypatch):
+    """Children equal to a parent inherit its fitness (GaParams::f_known): the pre-pass skips them.
+    Every generation's cached fitness vector equals a fresh classification of the population."""
+    from paper_2205_15311_b200.genome import SearchSpace, decode_tileset, genome_at_index
+    from paper_2205_15311_b200 import assembly as A
+    S28 = SearchSpace(2, 8)
+    tgt_idx = 0x801772
+    target = A.assemble_once(decode_tileset(genome_at_index(S28, tgt_idx), S28), 19, seed=0,
+                             genome_index=tgt_idx, run_index=0).grid.cells >= 0
+    n = 8192
+    ga = E.DeviceGA(n, 24, 0.3, mode)
+    ga.set_population(np.random.default_rng(9).integers(0, 1 << 24, n, dtype=np.uint64))
+    for g in range(5):
+        f = ga.jatam_fitness(S28, target, 19, 8).clone()
+        monkeypatch.setenv("TV_FITCACHE", "0")
+        fresh = ga.jatam_fitness(S28, target, 19, 8).clone()
+        monkeypatch.delenv("TV_FITCACHE")
+        assert bool((f == fresh).all()), g
+        ga.run(3, g, 1, 361, n, 0, f_ext=f)
+    ga.close()
