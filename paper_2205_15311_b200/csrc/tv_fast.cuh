@@ -329,10 +329,13 @@ template <bool S> struct Cand<1, S> : CandSwar<uint32_t, 8, S> {};
 enum { ST_NEED = 0, ST_RUN = 1, ST_DONE = 2 };
 
 // board layout of the fast kernel: row-aligned (a <= 2) or dense (a = 3), see k_classify_fast
-template <int A> __host__ __device__ constexpr bool fast_rows() { return A <= 2; }
+#ifndef TV_A3_ROWS
+#define TV_A3_ROWS 0  // a = 3 on the row-aligned board with the movelist ring too (A/B)
+#endif
+template <int A> __host__ __device__ constexpr bool fast_rows() { return A <= 2 || TV_A3_ROWS; }
 __host__ __device__ inline int fast_board_words(int a, int d) {
   const int PD = d + 2;
-  return a <= 2 ? PD * ((PD + 7) / 8) : (PD * PD + 7) / 8;
+  return (a <= 2 || TV_A3_ROWS) ? PD * ((PD + 7) / 8) : (PD * PD + 7) / 8;
 }
 
 #define TV_KEY_BITS 11  // width of the k_prepass behaviour key
@@ -366,10 +369,10 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
   const int words_per_warp = (GW + P.S / 2) * 32;
-  FastLane<A <= 2> Ln;
+  FastLane<fast_rows<A>()> Ln;  // the ring goes with the row-aligned board (less shared memory per lane)
   Ln.gw = smem + warp * words_per_warp + lane;
   Ln.sw = reinterpret_cast<uint16_t *>(smem + warp * words_per_warp + GW * 32) + lane;
-  Ln.mask = A <= 2 ? P.S - 1 : P.S;  // a <= 2: the host sizes the ring as a power of two
+  Ln.mask = fast_rows<A>() ? P.S - 1 : P.S;  // ring: the host sizes it as a power of two
   const int64_t gwarp = (int64_t)blockIdx.x * nwarps + warp;
   Ln.spill = P.spill + gwarp * (int64_t)P.spill_cap * 32 + lane;
   uint32_t *rh = P.run_hash + gwarp * (int64_t)P.kmax * 32 + lane;  // run r at rh[r*32]
