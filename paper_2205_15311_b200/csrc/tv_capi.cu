@@ -308,7 +308,7 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
           if (want_order) {  // counting sort of the items by their behaviour key
             k_key_binscan<<<kNumKeys, 1024, 0, st>>>(tile_hist, ntiles, bintot);
             k_key_basescan<<<1, 1024, 0, st>>>(bintot);
-            k_key_scatter<<<(unsigned)ntiles, 256, 0, st>>>(key, iota, tile_hist, ntiles, bintot, P.n, order);
+            k_key_scatter<<<(unsigned)ntiles, 1024, 0, st>>>(key, iota, tile_hist, ntiles, bintot, P.n, order);
             CK(cudaGetLastError());
           }
           P.tf_flags = ff_flags;

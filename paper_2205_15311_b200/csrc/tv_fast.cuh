@@ -1009,7 +1009,7 @@ __global__ void __launch_bounds__(1024) k_key_basescan(uint32_t *bintot) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_key_scatter(const uint16_t *key, const uint32_t *iota,
+__global__ void __launch_bounds__(1024) k_key_scatter(const uint16_t *key, const uint32_t *iota,
                                                      const uint32_t *tile_hist, int64_t ntiles,
                                                      const uint32_t *binbase, int64_t n, uint32_t *order) {
   __shared__ uint32_t cur[kNumKeys];
