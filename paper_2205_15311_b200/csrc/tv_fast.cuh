@@ -770,8 +770,8 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
 // code), two optional products:
 //  * flags: trivial-freedom bits for the early unbound cut-off, bit (i & 31) of
 //    flags[i >> 5] for work item i (CandSwar::trivial_free);
-//  * key: a 10-bit behaviour key per genome; the items are stably
-//    radix-sorted by it, so (1) line-prone genomes (a tile bonds a copy of itself
+//  * key: an 11-bit behaviour key per genome (the lowest bit: trivial freedom); the
+//    items are counting-sorted by it (k_key_* below), so (1) line-prone genomes (a tile bonds a copy of itself
 //    through opposite faces: long UNBOUND runs -- in S_{2,8} 33 % of the genomes,
 //    45 % of the pops, 98 % of the slowest 0.1 %) run first and the kernel's tail
 //    is made of short genomes, and (2) the lanes of a warp hold genomes of the same
