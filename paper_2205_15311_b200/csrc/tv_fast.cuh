@@ -1021,8 +1021,15 @@ __global__ void __launch_bounds__(1024) k_key_scatter(const uint16_t *key, const
   for (int64_t base = t0 + (threadIdx.x & ~31); base < t1; base += blockDim.x) {
     const int64_t item = base + lane;
     const bool valid = item < t1;
-    const uint32_t k = valid ? key[item] : 0xFFFFFFFFu;
-    const unsigned peers = __match_any_sync(0xFFFFFFFFu, k);
+    const uint32_t k = valid ? key[item] : 0u;
+    // lanes holding the same key: one ballot per key bit (cheaper than __match_any_sync here)
+    unsigned peers = __ballot_sync(0xFFFFFFFFu, valid);
+#pragma unroll
+    for (int b = 0; b < TV_KEY_BITS; b++) {
+      const bool bit = (k >> b) & 1u;
+      const unsigned m = __ballot_sync(0xFFFFFFFFu, bit);
+      peers &= bit ? m : ~m;
+    }
     const int leader = __ffs(peers) - 1;
     uint32_t pos = 0;
     if (valid && lane == leader) pos = atomicAdd(&cur[k], (uint32_t)__popc(peers));

@@ -238,12 +238,14 @@ def test_spec_discovery_le_adaptation_1000_runs():
 
 
 @pytest.mark.gpu
-def test_jatam_fitness_matches_cpu():
-    """Device JaTAM-shape fitness == d^2 - shapediff(target, run-0 grid) for DET genomes (oracle)."""
+@pytest.mark.parametrize("d", [19, 17])
+def test_jatam_fitness_matches_cpu(d):
+    """Device JaTAM-shape fitness == d^2 - shapediff(target, run-0 grid) for DET genomes (oracle);
+    d = 19 runs the compile-time-geometry fitness kernel, d = 17 the run-time one."""
     from paper_2205_15311_b200._kernels import edges_from_labels
     from paper_2205_15311_b200.genome import SearchSpace, decode_tileset, genome_at_index
     S28 = SearchSpace(2, 8)
-    d, k = 19, 8
+    k = 8
     # target: the run-0 grid of a 12-cell deterministic genome
     tgt_idx = 0x801772
     ts = decode_tileset(genome_at_index(S28, tgt_idx), S28)
