@@ -279,7 +279,7 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
       uint16_t *key = nullptr;
       unsigned long long *n_skip = nullptr;
       if (want_onemer) CK(S.get(&n_skip, 1));
-      const int64_t nwmax = (smax + 31) / 32, ntmax = (smax + kKeyTile - 1) / kKeyTile;
+      const int64_t nwmax = (smax + 31) / 32, ntmax = (smax + 1023) / 1024;  // key_tile_for() >= 1024
       if (want_flags) CK(S.get(&flags, (size_t)nwmax));
       if (want_order) {  // counting sort by key (k_prepass tile histograms + k_key_*), no library sort
         CK(S.get(&order, (size_t)smax)); CK(S.get(&iota, (size_t)smax)); CK(S.get(&key, (size_t)smax));
@@ -299,16 +299,17 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
         if (off > 0) CK(cudaMemsetAsync(work, 0, sizeof(unsigned long long), st));
         if (n_skip) CK(cudaMemsetAsync(n_skip, 0, sizeof(unsigned long long), st));
         if (want_flags || want_order) {
-          int64_t ntiles = (P.n + kKeyTile - 1) / kKeyTile;
+          int64_t tile = key_tile_for(P.n, nsm);
+          int64_t ntiles = (P.n + tile - 1) / tile;
           uint16_t *kk = want_order ? key : nullptr;
           uint32_t *ff_flags = want_flags ? flags : nullptr;
           uint32_t *th = want_order ? tile_hist : nullptr;
-          void *fargs[] = {&P, &ff_flags, &kk, &iota, &n_skip, &th, &ntiles};
+          void *fargs[] = {&P, &ff_flags, &kk, &iota, &n_skip, &th, &ntiles, &tile};
           CK(cudaLaunchKernel(ff, dim3((unsigned)ntiles), dim3(256), fargs, 0, st));
           if (want_order) {  // counting sort of the items by their behaviour key
             k_key_binscan<<<kNumKeys, 1024, 0, st>>>(tile_hist, ntiles, bintot);
             k_key_basescan<<<1, 1024, 0, st>>>(bintot);
-            k_key_scatter<<<(unsigned)ntiles, 1024, 0, st>>>(key, iota, tile_hist, ntiles, bintot, P.n, order);
+            k_key_scatter<<<(unsigned)ntiles, 1024, 0, st>>>(key, iota, tile_hist, ntiles, bintot, P.n, tile, order);
             CK(cudaGetLastError());
           }
           P.tf_flags = ff_flags;

@@ -794,12 +794,19 @@ constexpr uint16_t kOneMerKey = (1u << TV_KEY_BITS) - 1u;
 //    _scatter below, no library sort): CTA b handles the tile of items [b TILE, (b+1) TILE) and
 //    writes the tile's key histogram to tile_hist[key * ntiles + b].
 constexpr int kNumKeys = 1 << TV_KEY_BITS;
-constexpr int kKeyTile = 16384;  // items per pre-pass / scatter CTA (multiple of 32)
+// items per pre-pass / scatter CTA: a multiple of 32, sized by the host so that even small
+// launches get a few CTAs per SM (key_tile_for)
+inline int64_t key_tile_for(int64_t n, int nsm) {
+  int64_t t = (n + 4 * (int64_t)nsm - 1) / (4 * (int64_t)nsm);
+  t = (t + 31) / 32 * 32;
+  return t < 1024 ? 1024 : t;
+}
 
 template <int A, bool STRICT>
 __global__ void __launch_bounds__(256, TV_PREPASS_MINB) k_prepass(const __grid_constant__ ClassifyParams P, uint32_t *flags,
                                                  uint16_t *key_out, uint32_t *iota_out,
-                                                 unsigned long long *n_skip, uint32_t *tile_hist, int64_t ntiles) {
+                                                 unsigned long long *n_skip, uint32_t *tile_hist, int64_t ntiles,
+                                                 int64_t tile) {
   constexpr int NC = 4 * A;
   const int lane = threadIdx.x & 31;
   __shared__ unsigned long long s_om_min;
@@ -809,7 +816,7 @@ __global__ void __launch_bounds__(256, TV_PREPASS_MINB) k_prepass(const __grid_c
   if (tile_hist)
     for (int b = threadIdx.x; b < kNumKeys; b += blockDim.x) s_hist[b] = 0u;
   __syncthreads();
-  const int64_t t0 = (int64_t)blockIdx.x * kKeyTile, t1 = min(P.n, t0 + kKeyTile);
+  const int64_t t0 = (int64_t)blockIdx.x * tile, t1 = min(P.n, t0 + tile);
   for (int64_t base = t0 + (threadIdx.x & ~31); base < t1; base += blockDim.x) {
     const int64_t item = base + lane;
     bool f = false, om = false;
@@ -1011,13 +1018,14 @@ __global__ void __launch_bounds__(1024) k_key_basescan(uint32_t *bintot) {
 
 __global__ void __launch_bounds__(1024) k_key_scatter(const uint16_t *key, const uint32_t *iota,
                                                      const uint32_t *tile_hist, int64_t ntiles,
-                                                     const uint32_t *binbase, int64_t n, uint32_t *order) {
+                                                     const uint32_t *binbase, int64_t n, int64_t tile,
+                                                     uint32_t *order) {
   __shared__ uint32_t cur[kNumKeys];
   for (int b = threadIdx.x; b < kNumKeys; b += blockDim.x)
     cur[b] = binbase[b] + tile_hist[(int64_t)b * ntiles + blockIdx.x];
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int64_t t0 = (int64_t)blockIdx.x * kKeyTile, t1 = min(n, t0 + kKeyTile);
+  const int64_t t0 = (int64_t)blockIdx.x * tile, t1 = min(n, t0 + tile);
   for (int64_t base = t0 + (threadIdx.x & ~31); base < t1; base += blockDim.x) {
     const int64_t item = base + lane;
     const bool valid = item < t1;
