@@ -199,6 +199,15 @@ int tv_ga_fitness_jatam(tv_ga *h, int32_t a, int32_t bpl, const int64_t *mask_po
                         int64_t m, const int64_t *free_pos, int64_t nfree, int32_t d, int32_t k, uint64_t seed,
                         int32_t strict, const uint8_t *target_occ, uint32_t *f_out, void *stream);
 
+/* n_gens JaTAM-fitness generations in one call, no early stop: each generation = the
+ * fitness of the current population (tv_ga_fitness_jatam semantics; children equal to a
+ * parent inherit its fitness) + one reproduction (tv_ga_run with f_ext, seed, generation
+ * g0 + t).  Stats per generation [h|d] (may be NULL).  Enqueued without host round trips;
+ * synchronises once at the end. */
+int tv_ga_run_jatam(tv_ga *h, int32_t a, int32_t bpl, const int64_t *mask_pos, const uint8_t *mask_val, int64_t m,
+                    const int64_t *free_pos, int64_t nfree, int32_t d, int32_t k, uint64_t fit_seed, int32_t strict,
+                    const uint8_t *target_occ, uint64_t seed, int64_t g0, int64_t n_gens, uint32_t target,
+                    uint32_t *best, uint64_t *sum, uint32_t *count, void *stream);
 /* SPEC ACCEPTANCE 8 mutation benchmark (orc_ga_mutate semantics): mutate the word-major
  * device population pop [W x n] of L-bit genomes in place with stream (seed, g, i);
  * method 0 = by distribution (the GA's operator, T host or device), 1 = bit by bit (one

@@ -77,6 +77,8 @@ _SIGS = {
                               _p, _p, _p, _p, _p]),
     "tv_ga_fitness_jatam": (_i32, [_p, _i32, _i32, _p, _p, _i64, _p, _i64, _i32, _i32, _u64, _i32, _p, _p, _p]),
     "tv_ga_mutate": (_i32, [_p, _i64, _i32, _p, _u64, _i32, _u64, _i64, _p, _p]),
+    "tv_ga_run_jatam": (_i32, [_p, _i32, _i32, _p, _p, _i64, _p, _i64, _i32, _i32, _u64, _i32, _p, _u64, _i64, _i64,
+                               ctypes.c_uint32, _p, _p, _p, _p]),
     "tv_int_peak_launch": (_i32, [_i64, _i32, _i32, _p, _p]),
     "tv_sm_count": (_i32, [_p]),
     "tv_l2_probe_launch": (_i32, [_p, _i64, _i32, _i32, _p, _p]),

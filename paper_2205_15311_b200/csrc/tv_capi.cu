@@ -1474,4 +1474,63 @@ int tv_ga_fitness_jatam(tv_ga *h, int32_t a, int32_t bpl, const int64_t *mask_po
   return launch_classify(C, S, st);
 }
 
+int tv_ga_run_jatam(tv_ga *h, int32_t a, int32_t bpl, const int64_t *mask_pos, const uint8_t *mask_val, int64_t m,
+                    const int64_t *free_pos, int64_t nfree, int32_t d, int32_t k, uint64_t fit_seed, int32_t strict,
+                    const uint8_t *target_occ, uint64_t seed, int64_t g0, int64_t n_gens, uint32_t target,
+                    uint32_t *best, uint64_t *sum, uint32_t *count, void *stream) {
+  NvtxRange nvtx_("tv_ga_run_jatam", (long long)n_gens);
+  if (!h) return fail(TV_ERR_ARG, "null GA");
+  if (h->W > 1) return fail(TV_ERR_ARG, "JaTAM fitness needs L <= 64");
+  if (n_gens < 1) return fail(TV_ERR_ARG, "n_gens must be >= 1");
+  if (d > 29) return fail(TV_ERR_ARG, "JaTAM fitness supports d <= 29");
+  if (nfree != h->P.L) return fail(TV_ERR_ARG, "GA genome length %d != %lld free bits", h->P.L, (long long)nfree);
+  if ((uint64_t)d * d * (uint64_t)h->P.n >= ((uint64_t)1 << 32)) return fail(TV_ERR_ARG, "d^2 * population must be < 2^32");
+  Common C0;
+  const int64_t ks[1] = {k};
+  if (int rc = fill_common(a, bpl, mask_pos, mask_val, m, free_pos, nfree, d, ks, 1, k, fit_seed, strict, C0)) return rc;
+  C0.P.fit_mode = 1;
+  int tc = 0;
+  for (int r = 0; r < d; r++)
+    for (int c = 0; c < d; c++)
+      if (target_occ[r * d + c]) { C0.P.target_rows[r + 1] |= 1u << (c + 1); tc++; }
+  C0.P.target_cells = tc;
+  C0.P.n = h->P.n;
+  cudaStream_t st = (cudaStream_t)stream;
+  Scratch S(st);
+  uint32_t *f, *d_best, *d_count; unsigned long long *d_sum;
+  CK(S.get(&f, (size_t)h->P.n));
+  CK(S.get(&d_best, n_gens)); CK(S.get(&d_count, n_gens)); CK(S.get(&d_sum, n_gens));
+  CK(cudaMemsetAsync(d_best, 0, n_gens * 4, st));
+  CK(cudaMemsetAsync(d_count, 0, n_gens * 4, st));
+  CK(cudaMemsetAsync(d_sum, 0, n_gens * 8, st));
+  const char *efc = getenv("TV_FITCACHE");
+  const bool cache = efc ? atoi(efc) != 0 : true;
+  // every generation reproduces (no stop rule), so the current buffer alternates on the host
+  // side without reading the device back: the whole call is enqueued in one go
+  for (int64_t t = 0; t < n_gens; t++) {
+    Common C = C0;
+    C.P.out_fit = f;
+    C.P.indices = reinterpret_cast<const uint64_t *>(h->cur ? h->P.pop1 : h->P.pop0);
+    C.P.fit_known = (h->fknown_valid && cache) ? h->fknown : nullptr;
+    {
+      Scratch SC(st);
+      if (int rc = launch_classify(C, SC, st)) return rc;
+    }
+    GaParams P = h->P;
+    if (h->cur) std::swap(P.pop0, P.pop1);
+    P.seed = seed; P.g0 = g0 + t; P.n_gens = 1; P.target = target; P.adapt_count = h->P.n; P.stop_when = 0;
+    P.fitness = 1; P.f_ext = f; P.f_known = h->fknown; P.prof = nullptr;
+    P.best = d_best + t; P.count = d_count + t; P.sum = d_sum + t;
+    void *args[] = {&P};
+    CK(cudaLaunchCooperativeKernel((const void *)k_ga_run, dim3(h->nblocks), dim3(TV_GA_THREADS), args, h->smem, st));
+    h->cur ^= 1;
+    h->fknown_valid = true;
+  }
+  if (best) CK(cudaMemcpyAsync(best, d_best, n_gens * 4, cudaMemcpyDefault, st));
+  if (count) CK(cudaMemcpyAsync(count, d_count, n_gens * 4, cudaMemcpyDefault, st));
+  if (sum) CK(cudaMemcpyAsync(sum, d_sum, n_gens * 8, cudaMemcpyDefault, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
 }  // extern "C"

@@ -265,6 +265,23 @@ class DeviceGA:
         k = done.value
         return k, best[:k], sm[:k], cnt[:k]
 
+    def run_jatam(self, space: SearchSpace, target_occ: np.ndarray, seed: int, g0: int, n_gens: int, target: int,
+                  d: int = 19, k: int = 8, fit_seed: int = 0, strict: bool = True, stream=None):
+        """n_gens JaTAM-fitness generations without early stop in one call (tv_ga_run_jatam: the
+        same generations as jatam_fitness + run(..., 1, ..., f_ext) repeated, enqueued without host
+        round trips).  Returns (best, sum, count) per generation."""
+        a, bpl, mp, mv, fp = space.kernel_args()
+        occ = np.ascontiguousarray(np.asarray(target_occ, dtype=bool).reshape(d * d), np.uint8)
+        best = np.zeros(n_gens, np.uint32)
+        sm = np.zeros(n_gens, np.uint64)
+        cnt = np.zeros(n_gens, np.uint32)
+        P = _lib.ptr
+        _lib.check(_lib.lib().tv_ga_run_jatam(self._h, a, bpl, P(mp), P(mv), mp.shape[0], P(fp), fp.shape[0], d, k,
+                                              int(np.uint64(fit_seed)), int(bool(strict)), P(occ),
+                                              int(np.uint64(seed)), int(g0), int(n_gens), int(target), P(best),
+                                              P(sm), P(cnt), stream))
+        return best, sm, cnt
+
     def jatam_fitness(self, space: SearchSpace, target_occ: np.ndarray, d: int = 19, k: int = 8, seed: int = 0,
                       strict: bool = True):
         """Device vector of JaTAM-shape fitness for the current population (enumeration indices)."""
@@ -339,6 +356,11 @@ def run_ga(cfg: GAConfig, fitness="fujiyama", seed: int = 0, chunk: int = 4096) 
         stop = {"never": 0, "discovery": 1, "adaptation": 2}[cfg.stop_when]
         bests, sums, cnts = [], [], []
         g = 0
+        if jatam and stop == 0:  # no stop rule: every generation in one enqueued call
+            b, sm_, c = ga.run_jatam(fitness.space, fitness.target_occ, seed, 0, cfg.cutoff, cfg.target, fitness.d,
+                                     fitness.k, fitness.seed, fitness.strict)
+            bests.append(b); sums.append(sm_); cnts.append(c)
+            g = cfg.cutoff
         while g < cfg.cutoff:
             if jatam:
                 f = ga.jatam_fitness(fitness.space, fitness.target_occ, fitness.d, fitness.k, fitness.seed,

@@ -494,3 +494,36 @@ def test_jatam_fitness_cache_is_exact(mode, monkeypatch):
         assert bool((f == fresh).all()), g
         ga.run(3, g, 1, 361, n, 0, f_ext=f)
     ga.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [3000, 8192])
+def test_run_jatam_equals_generation_by_generation(n):
+    """tv_ga_run_jatam (all generations enqueued at once) == jatam_fitness + run(f_ext) per generation:
+    same stats rows, same final population; run_ga(JatamFitness, stop_when='never') takes that path."""
+    from paper_2205_15311_b200 import assembly as A
+    from paper_2205_15311_b200.genome import SearchSpace, decode_tileset, genome_at_index
+    S28 = SearchSpace(2, 8)
+    tgt_idx = 0x801772
+    target = A.assemble_once(decode_tileset(genome_at_index(S28, tgt_idx), S28), 19, seed=0,
+                             genome_index=tgt_idx, run_index=0).grid.cells >= 0
+    init = np.random.default_rng(n).integers(0, 1 << 24, n, dtype=np.uint64)
+    init[:7] = tgt_idx
+    gens = 6
+    g1 = E.DeviceGA(n, 24, 0.5, "asexual")
+    g1.set_population(init)
+    b1, s1, c1 = g1.run_jatam(S28, target, 13, 0, gens, 300)
+    g2 = E.DeviceGA(n, 24, 0.5, "asexual")
+    g2.set_population(init)
+    rows = []
+    for g in range(gens):
+        f = g2.jatam_fitness(S28, target, 19, 8)
+        rows.append(g2.run(13, g, 1, 300, n, 0, f_ext=f)[1:])
+    assert np.array_equal(b1, np.concatenate([r[0] for r in rows]))
+    assert np.array_equal(s1, np.concatenate([r[1] for r in rows]))
+    assert np.array_equal(c1, np.concatenate([r[2] for r in rows]))
+    assert np.array_equal(g1.population(), g2.population())
+    rec = E.run_ga(E.GAConfig(pop_size=n, length=24, mu_L=0.5, cutoff=gens, target=300, stop_when="never",
+                              init=init), fitness=E.JatamFitness(S28, target), seed=13)
+    assert np.array_equal(rec.best, b1) and np.array_equal(rec.count_at_target, c1)
+    g1.close(); g2.close()
