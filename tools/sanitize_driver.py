@@ -2,7 +2,8 @@
 synccheck / initcheck): classify_batch (pre-pass + sort + k_classify_fast, generic kernel),
 histogram mode (k_prepass, k_classify_fast, k_hist_* merge / export / payload fix-up), the
 device-row exchange (tv_hist_pack / replace_rows), canonical labels, the single-genome kernels,
-the GA (k_ga_run, k_ga_replicas, JaTAM fitness).  Sizes are small so racecheck finishes.
+the GA (k_ga_run, k_ga_replicas, JaTAM fitness and the fused JaTAM generations, wide genomes,
+the mutation benchmark).  Sizes are small so racecheck finishes.
 
 usage: compute-sanitizer --tool racecheck python tools/sanitize_driver.py
 """
@@ -54,4 +55,13 @@ tgt = A.assemble_once(t, 19, seed=0, genome_index=0x801772).grid.cells >= 0
 E.run_ga(E.GAConfig(pop_size=4096, length=24, mu_L=0.3, cutoff=3, stop_when="never",
                     init=np.random.default_rng(3).integers(0, 1 << 24, 4096, dtype=np.uint64)),
          fitness=E.JatamFitness(S28, tgt), seed=3)
+ga = E.DeviceGA(4096, 24, 0.3, "asexual")  # fused JaTAM generations (pre-pass fitness cache, counting sort)
+ga.set_population(np.random.default_rng(4).integers(0, 1 << 24, 4096, dtype=np.uint64))
+ga.run_jatam(S28, tgt, 5, 0, 3, 300)
+ga.close()
+E.run_ga(E.GAConfig(pop_size=2048, length=100, mu_L=1.0, mode="single_point", cutoff=5, stop_when="never"), seed=6)
+import torch  # noqa: E402
+pop = torch.zeros(16 * 2048, dtype=torch.int64, device="cuda")
+E.mutate_population(pop, 1024, 0.5, "distribution", count_flips=True)
+E.mutate_population(pop, 1024, 0.5, "bitwise", count_flips=True)
 print("GA ok", flush=True)
