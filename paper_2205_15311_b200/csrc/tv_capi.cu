@@ -1116,23 +1116,34 @@ int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **
   GaParams &P = h->P;
   P.n = n; P.L = L; P.mode = mode;
   for (int j = 0; j < 64; j++) P.T[j] = j < L ? T[j] : ~0ULL;
-  h->smem = 0;
-  int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ga_run, TV_GA_THREADS, h->smem));
-  if (per_sm < 1) { delete h; return fail(TV_ERR_CUDA, "GA kernel does not fit one CTA per SM"); }
   h->nblocks = nsm;
   if (const char *ec = getenv("TV_GA_CTAS")) h->nblocks = std::max(1, std::min(nsm, atoi(ec)));  // A/B only
   P.chunk = ((n + h->nblocks - 1) / h->nblocks + 31) / 32 * 32;  // whole rows of 32 (k_ga_run)
+  {  // staged mode: the chunk's genomes, fitness and row offsets in shared memory (k_ga_run)
+    const size_t bytes = (size_t)(2 * P.chunk + P.chunk / 32) * 4;
+    const char *es = getenv("TV_GA_STG"), *ep = getenv("TV_GA_PAIR");  // A/B only
+    P.stg = L <= 32 && bytes <= (size_t)200 * 1024 && (es ? atoi(es) != 0 : true);
+    P.pair = ep ? atoi(ep) != 0 : 1;
+    h->smem = P.stg ? bytes : 0;
+    static bool attr = false;  // once per process, at the cap (handles differ in chunk size)
+    if (P.stg && !attr) {
+      CK(cudaFuncSetAttribute(k_ga_run, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+  }
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ga_run, TV_GA_THREADS, h->smem));
+  if (per_sm < 1) { delete h; return fail(TV_ERR_CUDA, "GA kernel does not fit one CTA per SM"); }
   h->device = dev;
   h->cur = 0;
   cudaError_t e = cudaSuccess;
   {  // one arena for the generation loop's buffers
     const size_t al = 4096;
-    const size_t sz[10] = {(size_t)n * 8, (size_t)n * 8, (size_t)n * 4, (size_t)n * sizeof(ulonglong2), (size_t)n * 4,
+    const size_t sz[11] = {(size_t)n * 8, (size_t)n * 8, (size_t)n * 4, (size_t)n * sizeof(ulonglong2), (size_t)n * 4,
                           (size_t)h->nblocks * 8, (size_t)h->nblocks * (size_t)(P.chunk / 32) * 4, 8, 4,
-                          (size_t)n * 4};
-    size_t off[10], total = 0;
-    for (int i = 0; i < 10; i++) { off[i] = total; total += (sz[i] + al - 1) / al * al; }
+                          (size_t)n * 4, (size_t)h->nblocks * 4};
+    size_t off[11], total = 0;
+    for (int i = 0; i < 11; i++) { off[i] = total; total += (sz[i] + al - 1) / al * al; }
     auto bind = [&](char *base) {
       h->arena = base;
       P.pop0 = reinterpret_cast<unsigned long long *>(base + off[0]);
@@ -1145,6 +1156,7 @@ int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **
       P.done = reinterpret_cast<unsigned long long *>(base + off[7]);
       P.final_buf = reinterpret_cast<int32_t *>(base + off[8]);
       h->fknown = reinterpret_cast<uint32_t *>(base + off[9]);
+      P.first_g = reinterpret_cast<uint32_t *>(base + off[10]);
     };
     // Placement calibration (large populations): the same loop runs ~8 % slower depending on
     // where its buffers land physically (tools/ga_placement.py), so two

@@ -59,7 +59,10 @@ struct GaParams {
   uint32_t *cdf;         // n
   uint32_t *fstage;      // n: fitness staged in index order (own chunk per CTA)
   ulonglong2 *guide;     // n buckets (first B used per generation): x = (cdf[j] << 32) | j,
-                         // y = genome j (packed mode, L <= 32)
+                         // y = genome j (packed mode, L <= 32) [| genome j + 1 << 32 (pair)]
+  int32_t stg;           // the CTA's chunk is staged in shared memory (popcount fitness, L <= 32)
+  int32_t pair;          // popcount fitness: guide entries carry genomes j and j + 1
+  uint32_t *first_g;     // pair + stg: per CTA, the genome of its chunk's first individual
   unsigned long long *tot;  // per CTA chunk totals
   uint32_t *rowx;        // per CTA, per row of 32 individuals: fitness sum, then its exclusive offset
   uint32_t *best;        // n_gens
@@ -141,13 +144,21 @@ __device__ __forceinline__ uint32_t ga_pick(const GaParams &P, uint32_t r, uint3
 // Packed mode (L <= 32): population words carry (cdf[j] << 32) | genome j and
 // the guide entry carries the owner's genome, so the selected parent itself is
 // returned: one L2 read when the bucket owner covers r, one more per step
-// (cdf and genome in the same word) otherwise.
+// (cdf and genome in the same word) otherwise.  With popcount fitness the entry's
+// high half carries genome j + 1 as well (its cdf follows from its popcount): the
+// owner misses r for ~47 % of the draws (r is uniform over the bucket, the owner
+// covers on average half of it), the pair for ~0.5 %.
 __device__ __forceinline__ uint64_t ga_pick_genome(const GaParams &P, const unsigned long long *pop, uint32_t r,
-                                                   uint32_t total, uint64_t mul, uint32_t &jo) {
+                                                   uint32_t total, uint64_t mul, uint32_t &jo, bool pair) {
   if (total == 0) { jo = r; return pop[r] & 0xFFFFFFFFull; }
   const ulonglong2 e = P.guide[(uint32_t)(((uint64_t)r * mul) >> 32)];
   uint32_t j = (uint32_t)e.x, c = (uint32_t)(e.x >> 32);
-  uint64_t g = e.y;
+  uint64_t g = e.y & 0xFFFFFFFFull;
+  if (c <= r && pair) {  // popcount fitness: the entry also carries genome j + 1, whose
+    g = e.y >> 32;                 // cdf is cdf[j] + popcount -- about half the draws end here
+    c += (uint32_t)__popcll(g);
+    j++;
+  }
   while (c <= r) {
     const unsigned long long v = pop[++j];
     c = (uint32_t)(v >> 32);
@@ -215,11 +226,20 @@ __global__ void __launch_bounds__(TV_GA_THREADS, 1) k_ga_run(const __grid_consta
   const int64_t c1 = min(P.n, c0 + P.chunk);
   const int64_t len = max((int64_t)0, c1 - c0);
   const int nrows = (int)((len + 31) >> 5);
-  uint32_t *rowx = P.rowx + (int64_t)blockIdx.x * (P.chunk >> 5);
+  const bool packed = P.L <= 32;
+  // Staged mode (popcount fitness, L <= 32, chunk fits shared memory): the CTA's individuals
+  // (genome, fitness) and row offsets live in shared memory between phase C and phase B, so
+  // phase B reads nothing from L2 and phase C stores nothing but its row statistics; the
+  // population words in global memory are written by phase B (cdf | genome) and, for the
+  // final population, after the loop.
+  extern __shared__ uint32_t ga_dyn[];
+  const bool stg = P.stg != 0 && packed && P.fitness == 0;
+  uint32_t *const sg = ga_dyn, *const sf = ga_dyn + P.chunk;
+  uint32_t *rowx = stg ? ga_dyn + 2 * P.chunk : P.rowx + (int64_t)blockIdx.x * (P.chunk >> 5);
   int cur = 0;
   int64_t t = 0;
   const uint64_t full = P.L == 64 ? ~0ULL : ((1ULL << P.L) - 1);
-  const bool packed = P.L <= 32;
+  const bool pair = packed && P.fitness == 0 && P.pair;  // guide entries carry genomes j and j + 1
   // fitness of the initial population, staged in index order, with its row sums and stats
   if (tid == 0) { s_best = 0; s_cnt = 0; }
   __syncthreads();
@@ -227,8 +247,16 @@ __global__ void __launch_bounds__(TV_GA_THREADS, 1) k_ga_run(const __grid_consta
     const int64_t i = c0 + (int64_t)r * 32 + lane;
     uint32_t f = 0;
     if (i < c1) {
-      f = P.fitness == 0 ? (uint32_t)__popcll(P.pop0[i] & full) : P.f_ext[i];
-      P.fstage[i] = f;
+      if (stg) {
+        const uint32_t g = (uint32_t)(P.pop0[i] & full);
+        f = (uint32_t)__popc(g);
+        sg[i - c0] = g;
+        sf[i - c0] = f;
+        if (pair && i == c0) P.first_g[blockIdx.x] = g;
+      } else {
+        f = P.fitness == 0 ? (uint32_t)__popcll(P.pop0[i] & full) : P.f_ext[i];
+        P.fstage[i] = f;
+      }
     }
     const uint32_t s = __reduce_add_sync(0xFFFFFFFFu, f), mx = __reduce_max_sync(0xFFFFFFFFu, f);
     const uint32_t nc = (uint32_t)__popc(__ballot_sync(0xFFFFFFFFu, f >= P.target && i < c1));
@@ -282,13 +310,41 @@ __global__ void __launch_bounds__(TV_GA_THREADS, 1) k_ga_run(const __grid_consta
     const uint64_t mul = total ? (nb << 32) / total : 0ull;
     if (blockIdx.x == 0 && tid == 0) P.sum[t] = s_total;
     if (s_stop) { t++; break; }
-    {
+    if (stg) {  // staged: the chunk's genomes and fitness come from shared memory
+      const uint32_t off = (uint32_t)s_off;
+      const int wstep = nt >> 5;
+      const uint32_t gnext = pair && c1 < P.n ? P.first_g[blockIdx.x + 1] : 0u;
+      for (int r = wid; r < nrows; r += wstep) {
+        const int l = r * 32 + lane;
+        const bool in = l < len;
+        const uint32_t f = in ? sf[l] : 0u, gi = in ? sg[l] : 0u;
+        uint32_t x = f;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+          if (lane >= o) x += y;
+        }
+        if (in) {
+          const uint32_t run = off + rowx[r] + x, prev = run - f;
+          pop[c0 + l] = ((unsigned long long)run << 32) | gi;
+          if (f) {  // own r in [prev, run): buckets whose first r falls in it
+            const uint32_t b0 = prev ? (uint32_t)(((uint64_t)(prev - 1) * mul) >> 32) + 1 : 0u;
+            const uint32_t b1 = (uint32_t)(((uint64_t)(run - 1) * mul) >> 32);
+            const uint32_t gn = pair ? (l + 1 < len ? sg[l + 1] : gnext) : 0u;
+            const ulonglong2 e = make_ulonglong2(((unsigned long long)run << 32) | (uint32_t)(c0 + l),
+                                                 ((unsigned long long)gn << 32) | gi);
+#pragma unroll 1
+            for (uint32_t b = b0; b <= b1; b++) P.guide[b] = e;
+          }
+        }
+      }
+    } else {
       const uint32_t off = (uint32_t)s_off;
       constexpr int RB = 2;  // rows whose loads are issued before any store (stores could alias them; 4 spills)
       const int wstep = nt >> 5;
       for (int k0 = wid; k0 < nrows; k0 += RB * wstep) {
         uint32_t fr[RB], bx[RB];
-        uint64_t gr[RB];
+        uint64_t gr[RB], gn[RB];  // genome i, genome i + 1 of the row's last lane (pair entries)
 #pragma unroll
         for (int u = 0; u < RB; u++) {
           const int r = k0 + u * wstep;
@@ -296,6 +352,8 @@ __global__ void __launch_bounds__(TV_GA_THREADS, 1) k_ga_run(const __grid_consta
           const bool in = r < nrows && i < c1;
           fr[u] = in ? P.fstage[i] : 0u;
           gr[u] = in && packed ? (pop[i] & 0xFFFFFFFFull) : 0ull;
+          // (the low half of a population word is never written in phase B: no race)
+          gn[u] = pair && lane == 31 && in && i + 1 < P.n ? (pop[i + 1] & 0xFFFFFFFFull) : 0ull;
           bx[u] = r < nrows ? rowx[r] : 0u;
         }
 #pragma unroll
@@ -311,13 +369,15 @@ __global__ void __launch_bounds__(TV_GA_THREADS, 1) k_ga_run(const __grid_consta
             if (lane >= o) x += y;
           }
           const uint32_t run = off + bx[u] + x, prev = run - f;
+          const uint64_t g1 = __shfl_down_sync(0xFFFFFFFFu, gr[u], 1);
           if (i < c1) {
             if (packed) pop[i] = ((unsigned long long)run << 32) | gr[u];
             else P.cdf[i] = run;
             if (f) {  // own r in [prev, run): buckets whose first r falls in it
               const int64_t b0 = prev ? (int64_t)(((uint64_t)(prev - 1) * mul) >> 32) + 1 : 0;
               const int64_t b1 = (int64_t)(((uint64_t)(run - 1) * mul) >> 32);
-              const ulonglong2 e = make_ulonglong2(((unsigned long long)run << 32) | (uint32_t)i, gr[u]);
+              const uint64_t hi = pair ? ((lane == 31 ? gn[u] : (i + 1 < c1 ? g1 : 0ull)) & full) << 32 : 0ull;
+              const ulonglong2 e = make_ulonglong2(((unsigned long long)run << 32) | (uint32_t)i, gr[u] | hi);
               for (int64_t b = b0; b <= b1; b++) P.guide[b] = e;
             }
           }
@@ -342,11 +402,11 @@ __global__ void __launch_bounds__(TV_GA_THREADS, 1) k_ga_run(const __grid_consta
       uint32_t pa[NI], pb[NI];              // parents' indices
       if (packed) {
 #pragma unroll
-        for (int u = 0; u < NI; u++) { ga_[u] = ga_pick_genome(P, pop, D[u].ra, total, mul, pa[u]); cv[u] = ga_[u]; }
+        for (int u = 0; u < NI; u++) { ga_[u] = ga_pick_genome(P, pop, D[u].ra, total, mul, pa[u], pair); cv[u] = ga_[u]; }
         if (P.mode != 0) {
 #pragma unroll
           for (int u = 0; u < NI; u++) {
-            gb_[u] = ga_pick_genome(P, pop, D[u].rb, total, mul, pb[u]);
+            gb_[u] = ga_pick_genome(P, pop, D[u].rb, total, mul, pb[u], pair);
             cv[u] = (cv[u] & D[u].top) | (gb_[u] & ~D[u].top);
           }
         }
@@ -371,11 +431,17 @@ __global__ void __launch_bounds__(TV_GA_THREADS, 1) k_ga_run(const __grid_consta
         uint32_t f = 0;
         if (iu < c1) {
           const uint64_t c = (cv[u] ^ D[u].flips) & full;
-          nxt[iu] = c;
-          if (P.fitness == 0) {
+          if (stg) {
+            f = (uint32_t)__popcll(c);
+            sg[iu - c0] = (uint32_t)c;
+            sf[iu - c0] = f;
+            if (pair && iu == c0) P.first_g[blockIdx.x] = (uint32_t)c;
+          } else if (P.fitness == 0) {
+            nxt[iu] = c;
             f = (uint32_t)__popcll(c);
             P.fstage[iu] = f;
           } else {
+            nxt[iu] = c;
             f = P.fstage[iu];  // external fitness stays that of the staged population
             if (P.f_known) {   // a child equal to a parent has that parent's (deterministic) fitness
               uint32_t fk = 0xFFFFFFFFu;
@@ -408,6 +474,10 @@ __global__ void __launch_bounds__(TV_GA_THREADS, 1) k_ga_run(const __grid_consta
     }
     grid.sync();
     if (prof) P.prof[2] += ga_clock() - tp0;
+  }
+  if (stg && t > 0) {  // the final population was staged: publish it
+    unsigned long long *fin = cur ? P.pop1 : P.pop0;
+    for (int l = tid; l < (int)len; l += nt) fin[c0 + l] = sg[l];
   }
   if (blockIdx.x == 0 && tid == 0) {
     *P.done = (unsigned long long)t;
