@@ -131,6 +131,45 @@ __device__ __forceinline__ ChildDraws ga_draws(const GaParams &P, uint64_t gkey,
   return D;
 }
 
+// ga_draws for L <= 32 (the same draws, 32-bit masks): the Poisson count compares the
+// first four thresholds without a loop (T[j] = ~0 for j >= L, so a compare past L is false
+// and k < 4 needs no further test); the loop continues only from k = 4.
+struct ChildDraws32 {
+  uint32_t ra, rb, top, flips;
+};
+__device__ __forceinline__ ChildDraws32 ga_draws32(const GaParams &P, uint64_t gkey, int64_t i, uint32_t total) {
+  ChildDraws32 D;
+  uint64_t s = mix64(gkey ^ (kMixA * ((uint64_t)i + 1)));
+  const int L = P.L;
+  const uint32_t full = L == 32 ? 0xFFFFFFFFu : ((1u << L) - 1u);
+  const uint64_t range = total ? (uint64_t)total : (uint64_t)P.n;
+  D.ra = (uint32_t)__umul64hi(ga_draw(s), range);
+  D.rb = 0;
+  D.top = full;
+  if (P.mode != 0) {
+    D.rb = (uint32_t)__umul64hi(ga_draw(s), range);
+    if (P.mode == 1) {
+      const uint32_t p = ga_below(s, (uint32_t)L);
+      D.top = p == 0 ? 0u : (full & ~((1u << (L - p)) - 1u));
+    } else {
+      D.top = full & ~(uint32_t)ga_draw(s);
+    }
+  }
+  const uint64_t u = ga_draw(s) >> 1;
+  int k = (int)(u >= P.T[0]) + (int)(u >= P.T[1]) + (int)(u >= P.T[2]) + (int)(u >= P.T[3]);
+  if (k == 4)
+    while (k < L && u >= P.T[k]) k++;
+  uint32_t chosen = 0;
+  for (int f = 0; f < k;) {
+    const uint32_t bit = 1u << (L - 1 - (int)ga_below(s, (uint32_t)L));
+    if (chosen & bit) continue;
+    chosen |= bit;
+    f++;
+  }
+  D.flips = chosen;
+  return D;
+}
+
 // roulette: first j with cdf[j] > r, from the guide entry of r's bucket; the
 // entry carries cdf[j] so a bucket whose owner covers r costs one load
 __device__ __forceinline__ uint32_t ga_pick(const GaParams &P, uint32_t r, uint32_t total, uint64_t mul) {
@@ -219,7 +258,7 @@ __global__ void __launch_bounds__(TV_GA_THREADS, 1) k_ga_run(const __grid_consta
   cg::grid_group grid = cg::this_grid();
   __shared__ uint32_t warp_sum[33];  // blockDim.x <= 1024
   __shared__ uint32_t s_best, s_cnt, s_carry;
-  __shared__ unsigned long long s_off, s_total;
+  __shared__ unsigned long long s_off, s_total, s_gkey;
   __shared__ int s_stop;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
   const int64_t c0 = (int64_t)blockIdx.x * P.chunk;  // P.chunk is a multiple of 32
@@ -298,6 +337,7 @@ __global__ void __launch_bounds__(TV_GA_THREADS, 1) k_ga_run(const __grid_consta
       if (lane == 0) {
         s_off = o;
         s_total = tt;
+        s_gkey = mix64(P.seed ^ (kGold * ((uint64_t)g + 1)));  // stream_state prefix (_k:45-48)
         const uint32_t c = *((volatile uint32_t *)&P.count[t]);
         s_stop = (P.stop_when == 1 && c >= 1u) || (P.stop_when == 2 && (int64_t)c >= P.adapt_count);
       }
@@ -386,12 +426,39 @@ __global__ void __launch_bounds__(TV_GA_THREADS, 1) k_ga_run(const __grid_consta
     }
     grid.sync();
     if (prof) { tp1 = ga_clock(); P.prof[1] += tp1 - tp0; tp0 = tp1; }
-    const uint64_t gkey = mix64(P.seed ^ (kGold * ((uint64_t)g + 1)));  // stream_state prefix (_k:45-48)
+    const uint64_t gkey = s_gkey;
     // ---- C: children, TV_GA_ILP at a time (draws first, then the dependent loads); warp w
     //      makes rows w, w + 32, ... so row sums / best / count of the next generation are
     //      warp reductions
     constexpr int NI = TV_GA_ILP;
-    for (int64_t i = c0 + tid; i < c0 + (int64_t)nrows * 32; i += NI * nt) {
+    if (stg) {  // staged (L <= 32, popcount): 32-bit draws, children into shared memory
+      const uint32_t full32 = (uint32_t)full;
+      for (int l = tid; l < nrows * 32; l += nt) {
+        uint32_t f = 0;
+        if (l < (int)len) {
+          const ChildDraws32 D = ga_draws32(P, s_gkey, c0 + l, total);
+          uint32_t ja, jb;
+          uint32_t c = (uint32_t)ga_pick_genome(P, pop, D.ra, total, mul, ja, pair);
+          if (P.mode != 0) {
+            const uint32_t gb = (uint32_t)ga_pick_genome(P, pop, D.rb, total, mul, jb, pair);
+            c = (c & D.top) | (gb & ~D.top);
+          }
+          c = (c ^ D.flips) & full32;
+          f = (uint32_t)__popc(c);
+          sg[l] = c;
+          sf[l] = f;
+          if (pair && l == 0) P.first_g[blockIdx.x] = c;
+        }
+        const uint32_t sm = __reduce_add_sync(0xFFFFFFFFu, f), mx = __reduce_max_sync(0xFFFFFFFFu, f);
+        const uint32_t nc = (uint32_t)__popc(__ballot_sync(0xFFFFFFFFu, f >= P.target && l < (int)len));
+        if (lane == 0) {
+          rowx[l >> 5] = sm;
+          atomicMax(&s_best, mx);
+          if (nc) atomicAdd(&s_cnt, nc);
+        }
+      }
+    }
+    for (int64_t i = c0 + tid; !stg && i < c0 + (int64_t)nrows * 32; i += NI * nt) {
       ChildDraws D[NI];
 #pragma unroll
       for (int u = 0; u < NI; u++) {
