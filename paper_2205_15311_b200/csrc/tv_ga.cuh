@@ -659,20 +659,29 @@ __global__ void __launch_bounds__(1024, 1) k_ga_replicas(const __grid_constant__
     if (s_stop) { t++; break; }
     __syncthreads();
     const uint64_t gkey = mix64(seed ^ (kGold * ((uint64_t)(P.g0 + t) + 1)));
-    for (int i = tid; i < n; i += nt) {
-      const ChildDraws D = ga_draws(P, gkey, i, total);
-      auto pick = [&](uint32_t r) -> uint32_t {
-        if (total == 0) return r;
-        int lo = 0, hi = n - 1;  // first j with cdf[j] > r (cdf[n-1] = total > r)
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (cdf[mid] > r) hi = mid; else lo = mid + 1;
-        }
-        return (uint32_t)lo;
-      };
-      uint64_t c = pop[pick(D.ra)];
-      if (P.mode != 0) c = (c & D.top) | (pop[pick(D.rb)] & ~D.top);
-      nxt[i] = (c ^ D.flips) & full;
+    auto pick = [&](uint32_t r) -> uint32_t {
+      if (total == 0) return r;
+      int lo = 0, hi = n - 1;  // first j with cdf[j] > r (cdf[n-1] = total > r)
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (cdf[mid] > r) hi = mid; else lo = mid + 1;
+      }
+      return (uint32_t)lo;
+    };
+    if (P.L <= 32) {  // the same draws with 32-bit masks (ga_draws32)
+      for (int i = tid; i < n; i += nt) {
+        const ChildDraws32 D = ga_draws32(P, gkey, i, total);
+        uint32_t c = (uint32_t)pop[pick(D.ra)];
+        if (P.mode != 0) c = (c & D.top) | ((uint32_t)pop[pick(D.rb)] & ~D.top);
+        nxt[i] = (c ^ D.flips) & (uint32_t)full;
+      }
+    } else {
+      for (int i = tid; i < n; i += nt) {
+        const ChildDraws D = ga_draws(P, gkey, i, total);
+        uint64_t c = pop[pick(D.ra)];
+        if (P.mode != 0) c = (c & D.top) | (pop[pick(D.rb)] & ~D.top);
+        nxt[i] = (c ^ D.flips) & full;
+      }
     }
     cur ^= 1;
     __syncthreads();
