@@ -314,8 +314,9 @@ def ga_bench(args, n: int = 1 << 20, gens: int = 2000, ceil: dict | None = None)
             "roofline": {"bound": "hbm", "achieved": 16.0 * n * k / dev_s / 1e9, "peak": hbm_peak(), "unit": "GB/s",
                          "frac": 16.0 * n * k / dev_s / 1e9 / hbm_peak(), "traffic": ga_traffic(),
                          "note": "16 B/individual/generation algorithmic (SURVEY 8d); working set L2-resident, so "
-                                 "the binding limits are the two grid barriers per generation and dependent "
-                                 "L2 reads in selection (DESIGN.md section 6)",
+                                 "the binding limits are the two grid barriers per generation, dependent "
+                                 "L2 reads in selection and the instruction issue of the random draws "
+                                 "(DESIGN.md section 6)",
                          "l2": None if not ceil else {
                              "measured": ceil, "source": "bench.py l2_ceilings(): tv_l2_probe_launch / "
                                                          "tv_gridsync_probe_launch on this GPU",
@@ -323,15 +324,15 @@ def ga_bench(args, n: int = 1 << 20, gens: int = 2000, ceil: dict | None = None)
                              "barrier_floor_us_per_generation": 2 * ceil["grid_sync_us"],
                              "frac_of_barrier_floor": 2 * ceil["grid_sync_us"] / (dev_s / k * 1e6),
                              # composite floor of this kernel's own traffic: two grid barriers + one random
-                             # 16-byte guide read per child at the random-L2 rate + the streamed bytes
-                             # (phase B: fitness 4 + packed word 8 read, word 8 + guide 16 written; phase C:
-                             # child 8 + fitness 4 written) at the streaming-L2 rate
+                             # 16-byte guide read per child at the random-L2 rate + the streamed bytes at
+                             # the streaming-L2 rate (staged mode: phase B writes the packed word 8 + guide
+                             # entry 16; phase C keeps the children in shared memory)
                              "composite_floor_us_per_generation": (
                                  2 * ceil["grid_sync_us"] + 16.0 * n / (ceil["l2_random16_gbs"] * 1e3)
-                                 + 48.0 * n / (ceil["l2_stream_gbs"] * 1e3)),
+                                 + 24.0 * n / (ceil["l2_stream_gbs"] * 1e3)),
                              "frac_of_composite_floor": (
                                  2 * ceil["grid_sync_us"] + 16.0 * n / (ceil["l2_random16_gbs"] * 1e3)
-                                 + 48.0 * n / (ceil["l2_stream_gbs"] * 1e3)) / (dev_s / k * 1e6)}},
+                                 + 24.0 * n / (ceil["l2_stream_gbs"] * 1e3)) / (dev_s / k * 1e6)}},
             "cpu_baseline": {"value": cg / cpu_s, "unit": "generations/s", "cores": os.cpu_count(),
                              "kind": "restatement (no reference GA exists)",
                              "sample": f"{cg} generations of 2^20 on oracle/tv_ga_oracle.c, OpenMP"}}

@@ -1158,17 +1158,24 @@ int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **
       h->fknown = reinterpret_cast<uint32_t *>(base + off[9]);
       P.first_g = reinterpret_cast<uint32_t *>(base + off[10]);
     };
-    // Placement calibration (large populations): the same loop runs ~8 % slower depending on
-    // where its buffers land physically (tools/ga_placement.py), so two
-    // arenas are tried on a short generation loop and the faster one is kept.  Results do not
-    // depend on it (TV_GA_CALIB=0 disables it).
+    // Placement calibration (large populations): the same loop runs at ~23, ~27 or ~29 us per
+    // generation at 2^20 depending on where its buffers land physically (about 30 % of arenas
+    // are fast, tools/ga_bench_order.py), so K arenas (TV_GA_CALIB=K,
+    // default 8; 0 or 1 disables) are timed on a short generation loop over a random population
+    // and the fastest is kept (~10 ms once per handle; evolve pools handles).  Results do not
+    // depend on it.
     const char *ec = getenv("TV_GA_CALIB");
-    const bool calib = n >= ((int64_t)1 << 16) && (ec ? atoi(ec) != 0 : true);
-    char *arena[2] = {nullptr, nullptr};
-    float ms[2] = {0.f, 0.f};
-    for (int a = 0; a < (calib ? 2 : 1) && e == cudaSuccess; a++) {
-      e = cudaMalloc(&arena[a], total);
-      if (e != cudaSuccess || !calib) break;
+    int K = ec ? atoi(ec) : 8;
+    K = std::max(1, std::min(K, 8));
+    if (n < ((int64_t)1 << 16) || (size_t)K * total > ((size_t)2 << 30)) K = 1;
+    char *arena[8] = {nullptr}, *gap[8] = {nullptr};
+    float ms[8] = {0.f};
+    const char *eg = getenv("TV_GA_CALIB_GAP");  // development aid: MiB allocated between arenas
+    const size_t gap_bytes = eg ? (size_t)atoi(eg) << 20 : 0;
+    for (int a = 0; a < K && e == cudaSuccess; a++) {
+      if (a && gap_bytes) e = cudaMalloc(&gap[a], gap_bytes);
+      e = e ? e : cudaMalloc(&arena[a], total);
+      if (e != cudaSuccess || K == 1) break;
       bind(arena[a]);
       GaParams Q = P;
       const int gens = 24;
@@ -1180,7 +1187,10 @@ int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **
       cudaEvent_t e0 = nullptr, e1 = nullptr;
       e = e ? e : cudaMalloc(&sb, (size_t)gens * 8);
       e = e ? e : cudaMalloc(&ss, (size_t)gens * 8);
-      e = e ? e : cudaMemset(Q.pop0, 0, n * 8);
+      if (e == cudaSuccess) {
+        k_ga_fill_random<<<(unsigned)((n + 255) / 256), 256>>>(Q.pop0, n, L);
+        e = cudaGetLastError();
+      }
       e = e ? e : cudaMemset(sb, 0, (size_t)gens * 8);
       e = e ? e : cudaMemset(ss, 0, (size_t)gens * 8);
       Q.best = sb; Q.count = sb + gens; Q.sum = ss;
@@ -1200,11 +1210,22 @@ int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **
       cudaFree(sb); cudaFree(ss);
     }
     if (e == cudaSuccess) {
-      const int keep = (calib && arena[1] && ms[1] < ms[0]) ? 1 : 0;
-      if (arena[1 - keep]) cudaFree(arena[1 - keep]);
+      int keep = 0;
+      for (int a = 1; a < K; a++)
+        if (arena[a] && ms[a] < ms[keep]) keep = a;
+      if (getenv("TV_GA_CALIB_LOG")) {
+        fprintf(stderr, "tv_ga_create calibration (us/gen):");
+        for (int a = 0; a < K; a++)
+          fprintf(stderr, " %.2f%s[%p]", ms[a] * 1e3 / 24, a == keep ? "*" : "", (void *)arena[a]);
+        fprintf(stderr, "\n");
+      }
+      for (int a = 0; a < K; a++) {
+        if (a != keep && arena[a]) cudaFree(arena[a]);
+        if (gap[a]) cudaFree(gap[a]);
+      }
       bind(arena[keep]);
     } else {
-      cudaFree(arena[0]); cudaFree(arena[1]);
+      for (int a = 0; a < K; a++) { cudaFree(arena[a]); cudaFree(gap[a]); }
       h->arena = nullptr;
     }
   }

@@ -819,6 +819,14 @@ __global__ void __launch_bounds__(256) k_gaw_children(const __grid_constant__ Ga
   }
 }
 
+// placement calibration input (tv_ga_create): a fixed pseudo-random population of L-bit genomes
+__global__ void k_ga_fill_random(unsigned long long *pop, int64_t n, int32_t L) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t full = L >= 64 ? ~0ULL : ((1ULL << L) - 1);
+  pop[i] = mix64((uint64_t)i * kGold + kMixA) & full;
+}
+
 // genome-major (host layout [n, W]) <-> word-major (device layout [W, n])
 __global__ void k_gaw_transpose(const unsigned long long *src, unsigned long long *dst, int64_t n, int32_t W,
                                 int32_t to_word_major) {
