@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(TV_GA_THREADS, 1) k_ga_run(const __grid_consta
 #pragma unroll
       for (int u = 0; u < NI; u++) {
         const int64_t iu = i + u * nt;
-        D[u] = iu < c1 ? ga_draws(P, gkey, iu, total) : D[0];
+        D[u] = iu < c1 ? ga_draws(P, gkey, iu, total) : ChildDraws{0u, 0u, 0ull, 0ull};  // r = 0: an in-range pick
       }
       uint64_t cv[NI], ga_[NI], gb_[NI];  // child before mutation, parents' genomes
       uint32_t pa[NI], pb[NI];              // parents' indices

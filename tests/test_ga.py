@@ -194,6 +194,18 @@ def test_device_ga_equals_restatement(n, L, mode, lam, stop):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("stg,pair", [("0", "1"), ("1", "0"), ("0", "0")])
+@pytest.mark.parametrize("n,L,mode,lam,stop", [(4096 + 3, 32, 1, 1.0, 0), (1000, 24, 2, 0.3, 1), (1 << 17, 30, 0, 0.3, 2)])
+def test_device_ga_layout_switches(monkeypatch, stg, pair, n, L, mode, lam, stop):
+    """k_ga_run's staged chunk (shared memory between the phases) and paired guide entries are
+    layout choices: with either off (TV_GA_STG / TV_GA_PAIR, read at create) the run is the
+    same restatement, bit for bit (the default run has both on: test above)."""
+    monkeypatch.setenv("TV_GA_STG", stg)
+    monkeypatch.setenv("TV_GA_PAIR", pair)
+    test_device_ga_equals_restatement(n, L, mode, lam, stop)
+
+
+@pytest.mark.gpu
 def test_fujiyama_regime_desk_scale():
     """SPEC ACCEPTANCE 4 (runs=25, pop=512, L=32, cutoff=20000)."""
     med = []

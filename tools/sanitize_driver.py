@@ -51,6 +51,7 @@ print("single-genome ok", flush=True)
 E.run_ga(E.GAConfig(pop_size=4096, length=32, mu_L=0.3, cutoff=20, stop_when="never"), seed=1)
 E.run_ga(E.GAConfig(pop_size=2048, length=48, mu_L=1.0, mode="uniform", cutoff=10, stop_when="never"), seed=2)
 E.run_replicas(E.GAConfig(pop_size=512, mu_L=0.3, cutoff=30, stop_when="never"), range(4))
+E.run_ga(E.GAConfig(pop_size=3000, length=20, mu_L=0.5, cutoff=50, stop_when="discovery"), seed=3)  # staged stop
 tgt = A.assemble_once(t, 19, seed=0, genome_index=0x801772).grid.cells >= 0
 E.run_ga(E.GAConfig(pop_size=4096, length=24, mu_L=0.3, cutoff=3, stop_when="never",
                     init=np.random.default_rng(3).integers(0, 1 << 24, 4096, dtype=np.uint64)),
