@@ -448,6 +448,18 @@ def ga_jatam_bench(n: int = 1 << 20, gens: int = 20, peak: float | None = None, 
     dev_s = e0.elapsed_time(e1) / 1e3
     pop_now = ga.population()
     ga.close()
+    # e2e: the public API (evolve.run_ga with a JatamFitness, no stop rule) from the same random
+    # host population: H2D of the initial population, all generations, D2H of the records
+    init = np.random.default_rng(11).integers(0, 1 << 24, n, dtype=np.uint64)
+    fit = E.JatamFitness(S28, target, 19, 8, 0, True)
+    cfg = E.GAConfig(pop_size=n, length=24, mu_L=0.3, cutoff=gens, target=19 * 19, stop_when="never", init=init)
+    E.run_ga(cfg, fitness=fit, seed=5)  # warm-up (handle creation; pooled afterwards)
+    e2e_runs = []
+    for _ in range(3):
+        t = time.perf_counter()
+        E.run_ga(cfg, fitness=fit, seed=5)
+        e2e_runs.append(time.perf_counter() - t)
+    e2e_s = statistics.median(e2e_runs)
     cpu = None
     if cpu_leg:
         # CPU leg: the pinned C restatement classifies a 2^16 sample of the current population at
@@ -484,6 +496,10 @@ def ga_jatam_bench(n: int = 1 << 20, gens: int = 20, peak: float | None = None, 
             "config": {"workload": "GA toward a 12-cell S_(2,8) target shape, population 2^20, L=24, k=8, d=19, "
                                    "muL=0.3, asexual, random initial population", "generations_timed": gens},
             "best_fitness_seen": best,
+            "e2e": {"value": gens / e2e_s, "unit": "generations/s", "h2d_bytes_per_step": 8 * n / gens,
+                    "d2h_bytes_per_step": 16, "api": "evolve.run_ga(fitness=JatamFitness)",
+                    "note": "host clock around the call, median of 3; the 2^20 x 8 B initial population is copied "
+                            "once per call (per-step bytes amortised over the generations)"},
             "note": "each generation = k_prepass + counting sort + k_classify_fast (fit mode; unmutated children "
                     "inherit their parent's fitness and are skipped) over 2^20 genomes + one k_ga_run generation, "
                     "all generations enqueued by one tv_ga_run_jatam call; CUDA events on the launch stream",
