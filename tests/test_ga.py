@@ -370,6 +370,60 @@ def test_jatam_generations_external_fitness_vs_restatement(mode):
     ga.close()
 
 
+@pytest.mark.gpu
+def test_jatam_s38_fitness_and_generations():
+    """SURVEY 8(d) config 4 with genomes in S_{3,8} (L = 36: the unpacked GA path, a = 3 fitness
+    kernel): device fitness == the oracle's d^2 - shapediff for DET genomes, and external-
+    fitness generations == the restatement's children."""
+    from paper_2205_15311_b200._kernels import edges_from_labels
+    from paper_2205_15311_b200.genome import SearchSpace, decode_tileset, genome_at_index
+    S38 = SearchSpace(3, 8)
+    d, k, n, L, lam = 19, 8, 2048, 36, 0.5
+    rng = np.random.default_rng(38)
+    grid = np.empty(d * d, np.int16)
+
+    def edges(idx):
+        ts = decode_tileset(genome_at_index(S38, idx), S38)
+        return edges_from_labels(np.array([v for t in ts.tiles for v in t], np.uint8), 3)
+
+    def det_cells(idx):
+        sw = np.zeros(6, np.uint64)
+        st, cls, *_ = O.classify_single(edges(idx), 3, d, k, 0, idx, True, sw)
+        if st != 0 or cls != 0:
+            return None
+        O.assemble_single(edges(idx), 3, d, 0, idx, 0, True, grid)
+        return (grid >= 0).reshape(d, d).copy()
+
+    tgt_idx, target = None, None
+    for idx in rng.integers(0, 1 << 36, 20000, dtype=np.uint64):  # a DET target with a few cells
+        occ = det_cells(int(idx))
+        if occ is not None and occ.sum() >= 4:
+            tgt_idx, target = int(idx), occ
+            break
+    assert target is not None
+    pop = rng.integers(0, 1 << 36, n, dtype=np.uint64)
+    pop[:16] = tgt_idx
+    ga = E.DeviceGA(n, L, lam, "asexual")
+    ga.set_population(pop)
+    f = ga.jatam_fitness(S38, target, d, k).cpu().numpy().view(np.uint32)
+    for i in range(n):
+        occ = det_cells(int(pop[i]))
+        exp = 0 if occ is None else d * d - int(np.count_nonzero(occ != target))
+        assert int(f[i]) == exp, (i, int(pop[i]))
+    assert int(f[0]) == d * d
+    T = E.poisson_thresholds(lam, L)
+    for g in range(3):
+        f = ga.jatam_fitness(S38, target, d, k)
+        fh = f.cpu().numpy().view(np.uint32).astype(np.uint64)
+        cdf = np.cumsum(fh).astype(np.uint64)
+        kk, b, s, c = ga.run(7, g, 1, 300, n, 0, f_ext=f)
+        assert kk == 1 and int(b[0]) == int(fh.max()) and int(s[0]) == int(fh.sum())
+        exp = np.array([O.ga_child(7, g, i, pop, cdf, L, 0, T) for i in range(n)], np.uint64)
+        pop = ga.population()
+        assert np.array_equal(pop, exp), g
+    ga.close()
+
+
 # ---------------------------------------------------------------- wide genomes (L > 64)
 def _wide_random(rng, n, L):
     W = (L + 63) // 64
