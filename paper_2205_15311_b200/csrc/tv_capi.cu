@@ -1074,7 +1074,64 @@ struct tv_ga {
   void *arena;  // narrow GA: one allocation holding P's buffers
   uint32_t *fknown;   // per individual of the current population: its fitness if known (GaParams::f_known)
   bool fknown_valid;  // fknown describes the current population
+  // JaTAM fitness memo (ClassifyParams::memo_*), allocated at the first fitness call; valid for
+  // the fitness parameters whose signature is memo_sig (cleared when they change)
+  unsigned long long *memo_keys;
+  uint32_t *memo_vals;
+  uint64_t memo_cap;
+  uint64_t memo_sig;
+  bool memo_clear;             // set_population started a new run: clear before the next use
+  // which fitness function fknown's values come from (the JaTAM parameter signature), so a
+  // fitness call with other parameters never inherits them
+  uint64_t fknown_sig;
+  uint64_t fit_sig_last;       // signature and output buffer of the last tv_ga_fitness_jatam call
+  const uint32_t *fit_out_last;
 };
+
+// FNV-1a over the parameters a JaTAM fitness value depends on (besides the genome)
+static uint64_t fit_signature(int32_t a, int32_t bpl, const int64_t *mask_pos, const uint8_t *mask_val, int64_t m,
+                              const int64_t *free_pos, int64_t nfree, int32_t d, int32_t k, uint64_t seed,
+                              int32_t strict, const uint8_t *target_occ) {
+  uint64_t h = 0xCBF29CE484222325ULL;
+  auto mix = [&h](const void *p, size_t nb) {
+    const unsigned char *c = static_cast<const unsigned char *>(p);
+    for (size_t i = 0; i < nb; i++) { h ^= c[i]; h *= 0x100000001B3ULL; }
+  };
+  mix(&a, 4); mix(&bpl, 4); mix(&m, 8); mix(&nfree, 8); mix(&d, 4); mix(&k, 4); mix(&seed, 8); mix(&strict, 4);
+  if (m > 0) { mix(mask_pos, (size_t)m * 8); mix(mask_val, (size_t)m); }
+  if (nfree > 0) mix(free_pos, (size_t)nfree * 8);
+  mix(target_occ, (size_t)d * d);
+  return h;
+}
+
+// Bind the handle's fitness memo to P (allocating it on first use, clearing it when the fitness
+// parameters changed); TV_FITMEMO=0 disables it.  Capacity: a power of two >= 8 n, <= 2^24 slots.
+static int memo_bind(tv_ga *h, uint64_t sig, ClassifyParams &P, cudaStream_t st) {
+  P.memo_keys = nullptr; P.memo_vals = nullptr; P.memo_mask = 0;
+  const char *em = getenv("TV_FITMEMO");
+  if (em && atoi(em) == 0) return 0;
+  if (!h->memo_keys) {
+    uint64_t cap = 1;
+    while (cap < 8 * (uint64_t)h->P.n && cap < ((uint64_t)1 << 24)) cap <<= 1;
+    cudaError_t e = cudaMalloc(&h->memo_keys, cap * 8);
+    e = e ? e : cudaMalloc(&h->memo_vals, cap * 4);
+    if (e != cudaSuccess) {
+      cudaFree(h->memo_keys); cudaFree(h->memo_vals);
+      h->memo_keys = nullptr; h->memo_vals = nullptr;
+      cudaGetLastError();
+      return 0;  // no memo: every genome is classified
+    }
+    h->memo_cap = cap;
+    h->memo_sig = ~sig;  // force the clear below
+  }
+  if (h->memo_sig != sig || h->memo_clear) {
+    CK(cudaMemsetAsync(h->memo_keys, 0, h->memo_cap * 8, st));
+    h->memo_sig = sig;
+    h->memo_clear = false;
+  }
+  P.memo_keys = h->memo_keys; P.memo_vals = h->memo_vals; P.memo_mask = h->memo_cap - 1;
+  return 0;
+}
 
 int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **out) {
   if (n < 2 || n > ((int64_t)1 << 28)) return fail(TV_ERR_ARG, "population %lld outside [2, 2^28]", (long long)n);
@@ -1246,6 +1303,7 @@ int tv_ga_destroy(tv_ga *h) {
     cudaFree(P.done); cudaFree(P.final_buf);
   }
   cudaFree(h->Tw); cudaFree(h->fw); cudaFree(h->cdfw); cudaFree(h->flags); cudaFree(h->donew); cudaFree(h->scan_tmp);
+  cudaFree(h->memo_keys); cudaFree(h->memo_vals);
   delete h;
   return 0;
 }
@@ -1254,6 +1312,7 @@ int tv_ga_set_population(tv_ga *h, const uint64_t *genomes, void *stream) {
   if (!h) return fail(TV_ERR_ARG, "null GA");
   cudaStream_t st = (cudaStream_t)stream;
   h->fknown_valid = false;
+  h->memo_clear = true;  // a new run: the fitness memo starts empty (a repeated run is re-classified)
   unsigned long long *dst = h->cur ? h->P.pop1 : h->P.pop0;
   const int64_t words = h->P.n * h->W;
   if (!genomes) {
@@ -1390,6 +1449,8 @@ int tv_ga_run(tv_ga *h, uint64_t seed, int64_t g0, int64_t n_gens, uint32_t targ
   CK(cudaStreamSynchronize(st));
   h->cur ^= fb;
   h->fknown_valid = f_ext && fb;  // a reproduced generation with external fitness wrote fknown
+  // its values are those of the last JaTAM fitness call if f_ext is that call's output
+  h->fknown_sig = f_ext == h->fit_out_last ? h->fit_sig_last : 0;
   if (gens_done) *gens_done = done;
   return 0;
 }
@@ -1502,7 +1563,11 @@ int tv_ga_fitness_jatam(tv_ga *h, int32_t a, int32_t bpl, const int64_t *mask_po
   P.indices = reinterpret_cast<const uint64_t *>(h->cur ? h->P.pop1 : h->P.pop0);
   P.n = h->P.n;
   const char *efc = getenv("TV_FITCACHE");  // 0: classify every genome (A/B)
-  P.fit_known = (h->fknown_valid && (efc ? atoi(efc) != 0 : true)) ? h->fknown : nullptr;
+  const uint64_t sig = fit_signature(a, bpl, mask_pos, mask_val, m, free_pos, nfree, d, k, seed, strict, target_occ);
+  P.fit_known = (h->fknown_valid && h->fknown_sig == sig && (efc ? atoi(efc) != 0 : true)) ? h->fknown : nullptr;
+  if (int rc = memo_bind(h, sig, P, st)) return rc;
+  h->fit_sig_last = sig;
+  h->fit_out_last = f_out;
   Scratch S(st);
   return launch_classify(C, S, st);
 }
@@ -1529,6 +1594,9 @@ int tv_ga_run_jatam(tv_ga *h, int32_t a, int32_t bpl, const int64_t *mask_pos, c
   C0.P.target_cells = tc;
   C0.P.n = h->P.n;
   cudaStream_t st = (cudaStream_t)stream;
+  const uint64_t sig = fit_signature(a, bpl, mask_pos, mask_val, m, free_pos, nfree, d, k, fit_seed, strict,
+                                     target_occ);
+  if (int rc = memo_bind(h, sig, C0.P, st)) return rc;
   Scratch S(st);
   uint32_t *f, *d_best, *d_count; unsigned long long *d_sum;
   CK(S.get(&f, (size_t)h->P.n));
@@ -1544,7 +1612,7 @@ int tv_ga_run_jatam(tv_ga *h, int32_t a, int32_t bpl, const int64_t *mask_pos, c
     Common C = C0;
     C.P.out_fit = f;
     C.P.indices = reinterpret_cast<const uint64_t *>(h->cur ? h->P.pop1 : h->P.pop0);
-    C.P.fit_known = (h->fknown_valid && cache) ? h->fknown : nullptr;
+    C.P.fit_known = (h->fknown_valid && h->fknown_sig == sig && cache) ? h->fknown : nullptr;
     {
       Scratch SC(st);
       if (int rc = launch_classify(C, SC, st)) return rc;
@@ -1558,6 +1626,7 @@ int tv_ga_run_jatam(tv_ga *h, int32_t a, int32_t bpl, const int64_t *mask_pos, c
     CK(cudaLaunchCooperativeKernel((const void *)k_ga_run, dim3(h->nblocks), dim3(TV_GA_THREADS), args, h->smem, st));
     h->cur ^= 1;
     h->fknown_valid = true;
+    h->fknown_sig = sig;
   }
   if (best) CK(cudaMemcpyAsync(best, d_best, n_gens * 4, cudaMemcpyDefault, st));
   if (count) CK(cudaMemcpyAsync(count, d_count, n_gens * 4, cudaMemcpyDefault, st));

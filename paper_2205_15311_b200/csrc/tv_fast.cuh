@@ -531,7 +531,9 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
           } else if (FIT) {  // GA JaTAM-shape fitness: d^2 - shapediff for DET, else 0
             const int hc = ended == RUN_OVERFLOW ? CLS_ERROR : class_at(P.hist_k, trivial_at, first_unbound, first_mismatch);
             const int diff = P.target_cells + (int)(fit0 & 0xFFFFu) - 2 * (int)(fit0 >> 16);
-            P.out_fit[item] = hc == CLS_DET ? (uint32_t)(dd - diff) : 0u;
+            const uint32_t fit = hc == CLS_DET ? (uint32_t)(dd - diff) : 0u;
+            P.out_fit[item] = fit;
+            if (P.memo_mask) memo_put(P, idx, fit);
             st = ST_NEED;
           } else if (ended == RUN_OVERFLOW) {  // _k:434-437
             if (!HIST) {
@@ -822,6 +824,7 @@ __global__ void __launch_bounds__(256, TV_PREPASS_MINB) k_prepass(const __grid_c
     bool f = false, om = false;
     const bool valid = item < t1;
     uint64_t idx = 0;
+    uint32_t fk = 0xFFFFFFFFu;      // fit mode: the item's known fitness (~0 = unknown)
     uint32_t kk_all = 0xFFFFFFFFu;  // this item's key for the tile histogram (none if invalid)
     if (valid) {
       idx = item_index(P.indices, P.start, P.chunk, P.stride, P.item0 + item);
@@ -858,10 +861,13 @@ __global__ void __launch_bounds__(256, TV_PREPASS_MINB) k_prepass(const __grid_c
         }
         kk = ((line ? 0u : 1u) << 9) | ((self0 ? 0u : 1u) << 8) | ((uint32_t)(4 - nb0) << 5) |
              ((selfr ? 0u : 1u) << 4) | (uint32_t)(8 - nbr);
-        // GA fitness mode: a genome whose fitness the GA generation already knows (a child equal
-        // to its parent, GaParams::f_known) is skipped like a 1-mer
-        const bool known = P.fit_mode && P.fit_known && P.fit_known[item] != 0xFFFFFFFFu;
-        om = n_skip != nullptr && (nb0 == 0 || known);
+        // GA fitness mode: a genome whose fitness is already known (a child equal to its parent,
+        // GaParams::f_known, or a genome in the fitness memo) is skipped like a 1-mer
+        if (P.fit_mode) {
+          fk = P.fit_known ? P.fit_known[item] : 0xFFFFFFFFu;
+          if (fk == 0xFFFFFFFFu && P.memo_mask && nb0 != 0) fk = memo_get(P, idx);
+        }
+        om = n_skip != nullptr && (nb0 == 0 || fk != 0xFFFFFFFFu);
       }
       if (flags && !om) {  // (1-mers never reach the fast kernel)
         Cand<A, STRICT> K;
@@ -877,7 +883,6 @@ __global__ void __launch_bounds__(256, TV_PREPASS_MINB) k_prepass(const __grid_c
         if (om && P.fit_mode) {  // known fitness, or that of a DET 1x1 genome: d^2 - shapediff(target, centre)
           const int cr = (P.d >> 1) + 1;
           const int ov = (int)((P.target_rows[cr] >> cr) & 1u);
-          const uint32_t fk = P.fit_known ? P.fit_known[item] : 0xFFFFFFFFu;
           P.out_fit[item] = fk != 0xFFFFFFFFu ? fk : (uint32_t)(P.d * P.d - (P.target_cells + 1 - 2 * ov));
         } else if (om && !P.hist_mode) {  // classify_batch row of a DET 1x1 genome (_k:438-452)
           for (int k = 0; k < P.q; k++) P.out_class[item * P.q + k] = (uint8_t)CLS_DET;

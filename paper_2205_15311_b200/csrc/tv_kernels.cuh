@@ -28,6 +28,7 @@ __global__ void __launch_bounds__(128) k_classify_generic(const __grid_constant_
         fit = (uint32_t)(P.d * P.d - (P.target_cells + nc - 2 * ov));
       }
       P.out_fit[item] = fit;
+      if (P.memo_mask) memo_put(P, idx, fit);
       continue;
     }
     if (F.status != 0) {

@@ -42,6 +42,12 @@ struct ClassifyParams {
   int32_t target_cells;
   uint32_t *out_fit;
   const uint32_t *fit_known;  // per item: fitness known from the GA generation (~0 = unknown), or nullptr
+  // GA fitness memo (fit mode): open-addressed genome -> fitness table the GA handle keeps across
+  // generations while the fitness parameters stay the same; key = genome index + 1 (0 = empty).
+  // The pre-pass skips genomes found in it, the classify kernels insert what they compute.
+  unsigned long long *memo_keys;
+  uint32_t *memo_vals;
+  uint64_t memo_mask;       // capacity - 1 (a power of two), 0 = no memo
   uint32_t target_rows[32];
   // scratch
   uint32_t *run_hash;       // per lane, kmax entries
@@ -64,5 +70,37 @@ struct ClassifyParams {
   int32_t *g_placed;
   int64_t g_threads;
 };
+
+// GA fitness memo (ClassifyParams::memo_*): linear probing from a mixed slot, at most
+// kMemoProbes slots; a full neighbourhood only loses the memo entry, never exactness.
+constexpr int kMemoProbes = 16;
+__device__ __forceinline__ uint64_t memo_slot(uint64_t idx, uint64_t mask) {
+  return mix64(idx ^ 0xD1B54A32D192ED03ULL) & mask;
+}
+__device__ __forceinline__ uint32_t memo_get(const ClassifyParams &P, uint64_t idx) {
+  const unsigned long long key = idx + 1;
+  uint64_t s = memo_slot(idx, P.memo_mask);
+  for (int p = 0; p < kMemoProbes; p++) {
+    const unsigned long long k = P.memo_keys[s];
+    if (k == key) return P.memo_vals[s];
+    if (k == 0ULL) break;
+    s = (s + 1) & P.memo_mask;
+  }
+  return 0xFFFFFFFFu;
+}
+// values are read only by later launches (the next generation's pre-pass); two inserts of
+// one genome in a launch store the same value
+__device__ __forceinline__ void memo_put(const ClassifyParams &P, uint64_t idx, uint32_t fit) {
+  const unsigned long long key = idx + 1;
+  uint64_t s = memo_slot(idx, P.memo_mask);
+  for (int p = 0; p < kMemoProbes; p++) {
+    const unsigned long long prev = atomicCAS(&P.memo_keys[s], 0ULL, key);
+    if (prev == 0ULL || prev == key) {
+      P.memo_vals[s] = fit;
+      return;
+    }
+    s = (s + 1) & P.memo_mask;
+  }
+}
 
 }  // namespace tvb

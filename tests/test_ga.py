@@ -555,9 +555,47 @@ def test_jatam_fitness_cache_is_exact(mode, monkeypatch):
     for g in range(5):
         f = ga.jatam_fitness(S28, target, 19, 8).clone()
         monkeypatch.setenv("TV_FITCACHE", "0")
+        monkeypatch.setenv("TV_FITMEMO", "0")
         fresh = ga.jatam_fitness(S28, target, 19, 8).clone()
         monkeypatch.delenv("TV_FITCACHE")
+        monkeypatch.delenv("TV_FITMEMO")
         assert bool((f == fresh).all()), g
+        ga.run(3, g, 1, 361, n, 0, f_ext=f)
+    ga.close()
+
+
+@pytest.mark.gpu
+def test_jatam_fitness_memo_is_exact(monkeypatch):
+    """The genome -> fitness memo kept across generations (ClassifyParams::memo_*): a population
+    drawn from few distinct genomes hits it constantly; every fitness vector equals a fresh
+    classification, also after the fitness parameters change (target, k: the memo is cleared)."""
+    from paper_2205_15311_b200.genome import SearchSpace, decode_tileset, genome_at_index
+    from paper_2205_15311_b200 import assembly as A
+    S28 = SearchSpace(2, 8)
+
+    def shape(idx):
+        return A.assemble_once(decode_tileset(genome_at_index(S28, idx), S28), 19, seed=0,
+                               genome_index=idx, run_index=0).grid.cells >= 0
+    t1, t2 = shape(0x801772), shape(0x5A0013)
+    n = 6000
+    rng = np.random.default_rng(17)
+    pool = rng.integers(0, 1 << 24, 150, dtype=np.uint64)
+    ga = E.DeviceGA(n, 24, 0.5, "asexual")
+    ga.set_population(pool[rng.integers(0, pool.size, n)])
+
+    def fresh(target, k):
+        monkeypatch.setenv("TV_FITCACHE", "0")
+        monkeypatch.setenv("TV_FITMEMO", "0")
+        out = ga.jatam_fitness(S28, target, 19, k).clone()
+        monkeypatch.delenv("TV_FITCACHE")
+        monkeypatch.delenv("TV_FITMEMO")
+        return out
+    for g in range(6):
+        target, k = (t1, 8) if g < 3 else ((t2, 8) if g < 5 else (t2, 4))
+        f = ga.jatam_fitness(S28, target, 19, k).clone()
+        assert bool((f == fresh(target, k)).all()), g
+        again = ga.jatam_fitness(S28, target, 19, k).clone()  # the memo holds every genome now
+        assert bool((again == f).all()), g
         ga.run(3, g, 1, 361, n, 0, f_ext=f)
     ga.close()
 
