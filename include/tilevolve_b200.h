@@ -196,9 +196,10 @@ int tv_ga_replicas(int64_t n, int32_t L, int32_t mode, const uint64_t *T, int32_
  * the space: f = d^2 - shapediff(target, run-0 grid) if DET at k, else 0.
  * target_occ u8[d*d] host (seed-centred board); f_out device u32[n].  Exact reuse:
  * children equal to a parent inherit its fitness (after a tv_ga_run fed with this
- * call's f_out), and genomes met earlier in the run are looked up in a per-handle
- * genome -> fitness memo; both only under the same fitness parameters, and
- * tv_ga_set_population empties the memo (TV_FITCACHE=0 / TV_FITMEMO=0 disable). */
+ * call's f_out), and (populations >= 2^21) genomes met earlier in the run are
+ * looked up in a per-handle genome -> fitness memo; both only under the same
+ * fitness parameters, and tv_ga_set_population empties the memo (TV_FITCACHE=0
+ * disables the first, TV_FITMEMO=1/0 forces the memo on / off). */
 int tv_ga_fitness_jatam(tv_ga *h, int32_t a, int32_t bpl, const int64_t *mask_pos, const uint8_t *mask_val,
                         int64_t m, const int64_t *free_pos, int64_t nfree, int32_t d, int32_t k, uint64_t seed,
                         int32_t strict, const uint8_t *target_occ, uint32_t *f_out, void *stream);

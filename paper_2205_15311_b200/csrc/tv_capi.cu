@@ -1105,11 +1105,14 @@ static uint64_t fit_signature(int32_t a, int32_t bpl, const int64_t *mask_pos, c
 }
 
 // Bind the handle's fitness memo to P (allocating it on first use, clearing it when the fitness
-// parameters changed); TV_FITMEMO=0 disables it.  Capacity: a power of two >= 8 n, <= 2^24 slots.
+// parameters changed).  On by default for populations >= 2^21, where the fitness pass is
+// throughput-bound (below that it sits on its single-chain floor and the probes only cost:
+// DESIGN.md section 6); TV_FITMEMO=1 / 0 forces it on / off.  Capacity: a power of two
+// >= 8 n, <= 2^24 slots.
 static int memo_bind(tv_ga *h, uint64_t sig, ClassifyParams &P, cudaStream_t st) {
   P.memo_keys = nullptr; P.memo_vals = nullptr; P.memo_mask = 0;
   const char *em = getenv("TV_FITMEMO");
-  if (em && atoi(em) == 0) return 0;
+  if (em ? atoi(em) == 0 : h->P.n < ((int64_t)1 << 21)) return 0;
   if (!h->memo_keys) {
     uint64_t cap = 1;
     while (cap < 8 * (uint64_t)h->P.n && cap < ((uint64_t)1 << 24)) cap <<= 1;

@@ -577,6 +577,7 @@ def test_jatam_fitness_memo_is_exact(monkeypatch):
         return A.assemble_once(decode_tileset(genome_at_index(S28, idx), S28), 19, seed=0,
                                genome_index=idx, run_index=0).grid.cells >= 0
     t1, t2 = shape(0x801772), shape(0x5A0013)
+    monkeypatch.setenv("TV_FITMEMO", "1")  # on by default only from 2^21 individuals
     n = 6000
     rng = np.random.default_rng(17)
     pool = rng.integers(0, 1 << 24, 150, dtype=np.uint64)
@@ -588,7 +589,7 @@ def test_jatam_fitness_memo_is_exact(monkeypatch):
         monkeypatch.setenv("TV_FITMEMO", "0")
         out = ga.jatam_fitness(S28, target, 19, k).clone()
         monkeypatch.delenv("TV_FITCACHE")
-        monkeypatch.delenv("TV_FITMEMO")
+        monkeypatch.setenv("TV_FITMEMO", "1")
         return out
     for g in range(6):
         target, k = (t1, 8) if g < 3 else ((t2, 8) if g < 5 else (t2, 4))
