@@ -206,6 +206,31 @@ def test_device_ga_layout_switches(monkeypatch, stg, pair, n, L, mode, lam, stop
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("stg", ["1", "0"])
+def test_device_ga_zero_generations_and_immediate_stop(monkeypatch, stg):
+    """Edge cases of the staged loop: a call with no generations is refused, and a run that stops
+    at its first evaluation (target 0 is met at once) leaves the population as it was; the next
+    call continues exactly like the restatement."""
+    monkeypatch.setenv("TV_GA_STG", stg)
+    n, L, lam = 5000, 28, 0.7
+    init = np.random.default_rng(2).integers(0, 1 << L, n, dtype=np.uint64)
+    ga = E.DeviceGA(n, L, lam, "uniform")
+    ga.set_population(init)
+    with pytest.raises(ValueError):  # n_gens >= 1 (the reference loop evaluates at least once)
+        ga.run(4, 0, 0, 10, n, 0)
+    assert np.array_equal(ga.population(), init)
+    k, b, s, c = ga.run(4, 0, 50, 0, n, 1)  # count(f >= 0) = n >= 1: stop after recording generation 0
+    pop = init.copy()
+    k2, b2, s2, c2 = O.ga_run(pop, L, 2, E.poisson_thresholds(lam, L), 4, 0, 50, 0, n, 1)
+    assert k == k2 == 1 and np.array_equal(b, b2) and np.array_equal(c, c2)
+    assert np.array_equal(ga.population(), init) and np.array_equal(pop, init)
+    k, b, s, c = ga.run(4, 0, 7, 30, n, 0)
+    k2, b2, s2, c2 = O.ga_run(pop, L, 2, E.poisson_thresholds(lam, L), 4, 0, 7, 30, n, 0)
+    assert k == k2 == 7 and np.array_equal(s, s2) and np.array_equal(ga.population(), pop)
+    ga.close()
+
+
+@pytest.mark.gpu
 def test_fujiyama_regime_desk_scale():
     """SPEC ACCEPTANCE 4 (runs=25, pop=512, L=32, cutoff=20000)."""
     med = []
