@@ -226,7 +226,7 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
       while (P.S > 8 && 2 * (fast_smem_bytes(threads, P.GW, P.S, P.cta_slots, P.q) + 1024) > 228 * 1024) P.S -= 2;
     }
     P.S = std::max(4, std::min(P.S, (dd + 1) & ~1));
-    if (P.a <= 2 || TV_A3_ROWS) {  // the movelist ring (FastLane<true>::pop/push): power-of-two slots
+    if (P.a <= 2 || TV_A3_ROWS || TV_A3_RING) {  // the movelist ring (FastLane<true>): power-of-two slots
       int r = 4;
       while (2 * r <= P.S) r *= 2;
       P.S = r;

@@ -332,7 +332,11 @@ enum { ST_NEED = 0, ST_RUN = 1, ST_DONE = 2 };
 #ifndef TV_A3_ROWS
 #define TV_A3_ROWS 0  // a = 3 on the row-aligned board with the movelist ring too (A/B)
 #endif
+#ifndef TV_A3_RING
+#define TV_A3_RING 0  // a = 3 dense board with the movelist ring (A/B)
+#endif
 template <int A> __host__ __device__ constexpr bool fast_rows() { return A <= 2 || TV_A3_ROWS; }
+template <int A> __host__ __device__ constexpr bool fast_ring() { return fast_rows<A>() || TV_A3_RING; }
 __host__ __device__ inline int fast_board_words(int a, int d) {
   const int PD = d + 2;
   return (a <= 2 || TV_A3_ROWS) ? PD * ((PD + 7) / 8) : (PD * PD + 7) / 8;
@@ -369,10 +373,10 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
   const int words_per_warp = (GW + P.S / 2) * 32;
-  FastLane<fast_rows<A>()> Ln;  // the ring goes with the row-aligned board (less shared memory per lane)
+  FastLane<fast_ring<A>()> Ln;  // a <= 2: movelist ring; a = 3: linear stack (TV_A3_RING: ring)
   Ln.gw = smem + warp * words_per_warp + lane;
   Ln.sw = reinterpret_cast<uint16_t *>(smem + warp * words_per_warp + GW * 32) + lane;
-  Ln.mask = fast_rows<A>() ? P.S - 1 : P.S;  // ring: the host sizes it as a power of two
+  Ln.mask = fast_ring<A>() ? P.S - 1 : P.S;  // ring: the host sizes it as a power of two
   const int64_t gwarp = (int64_t)blockIdx.x * nwarps + warp;
   Ln.spill = P.spill + gwarp * (int64_t)P.spill_cap * 32 + lane;
   uint32_t *rh = P.run_hash + gwarp * (int64_t)P.kmax * 32 + lane;  // run r at rh[r*32]
