@@ -13,6 +13,13 @@ compute: ``enumerate`` is ``classify.enumerate_space`` (device histogram), ``ga`
 ``evolve.sweep`` (device replica kernel), ``render`` is ``assembly.classify_tileset``
 / ``assemble_once`` (one device thread).  Exit status 0 iff every output was written
 and the totals are consistent; any error prints one line to stderr and exits 2.
+
+Under ``torchrun`` (WORLD_SIZE > 1, one GPU per rank) ``enumerate`` shards the index
+range over the ranks (``distributed.enumerate_space_distributed``) and ``ga`` deals
+every sweep point's runs over them (``distributed.sweep_distributed``); rank 0 writes
+the outputs, which equal the single-GPU ones:
+
+    python -m torch.distributed.run --nproc-per-node 8 -m paper_2205_15311_b200 enumerate ...
 """
 from __future__ import annotations
 
@@ -111,6 +118,23 @@ def _parse_genome(text: str, space: SearchSpace) -> Genome:
     return g
 
 
+def _dist() -> tuple[int, int]:
+    """(rank, world); under torchrun joins the process group (NCCL, or TV_DIST_BACKEND) on
+    this rank's GPU."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world <= 1:
+        return 0, 1
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        if torch.cuda.is_available():  # (ranks share a GPU when there are fewer GPUs than ranks)
+            torch.cuda.set_device(local % torch.cuda.device_count())
+        backend = os.environ.get("TV_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
+        dist.init_process_group(backend)
+    return dist.get_rank(), dist.get_world_size()
+
+
 # ----------------------------------------------------------------------------- enumerate
 def cmd_enumerate(args) -> int:
     from .classify import enumerate_space
@@ -131,23 +155,35 @@ def cmd_enumerate(args) -> int:
         _check_writable(p)
     if args.resume and not os.path.isfile(args.resume):
         raise CliError(f"checkpoint {args.resume} not found")
+    rank, world = _dist()
     prog = None
-    if not args.quiet:
+    if not args.quiet and rank == 0:
         def prog(done, total):
             print(f"batches {done}/{total}", file=sys.stderr, flush=True)
     try:
-        h = enumerate_space(space, d=args.grid, seed=args.seed, batch_size=args.batch_size, workers=args.workers,
-                            ks=ks, hist_k=args.hist_k, strict=not args.no_strict, start=args.start, count=count,
-                            checkpoint=args.checkpoint, checkpoint_every=args.checkpoint_every,
-                            resume=args.resume, progress=prog)
+        if world > 1:
+            if args.checkpoint or args.resume:
+                raise CliError("--checkpoint / --resume are single-GPU options (a multi-GPU run is one pass)")
+            from .distributed import enumerate_space_distributed
+            h = enumerate_space_distributed(space, d=args.grid, seed=args.seed, batch_size=args.batch_size,
+                                            ks=ks, hist_k=args.hist_k, strict=not args.no_strict,
+                                            start=args.start, count=count)
+        else:
+            h = enumerate_space(space, d=args.grid, seed=args.seed, batch_size=args.batch_size,
+                                workers=args.workers, ks=ks, hist_k=args.hist_k, strict=not args.no_strict,
+                                start=args.start, count=count, checkpoint=args.checkpoint,
+                                checkpoint_every=args.checkpoint_every, resume=args.resume, progress=prog)
     except (ValueError, OSError) as e:  # corrupt / mismatched checkpoint, range errors
         raise CliError(str(e)) from None
     tallies = h.tallies
     if not all(int(r.sum()) == count for r in tallies):
         raise CliError(f"inconsistent totals: per-k sums {tallies.sum(axis=1).tolist()} != {count}")
+    if rank != 0:  # every rank holds the merged histogram; rank 0 writes it
+        return 0
     h.to_csv(args.out, space=space)
     summ = h.summary()
-    summ["params"] = {k: v for k, v in summ["params"].items() if k != "runtime_s"}
+    # runtime plumbing (wall time, number of ranks) is not part of what the run computes
+    summ["params"] = {k: v for k, v in summ["params"].items() if k not in ("runtime_s", "world")}
     summ["total"] = h.total
     with open(summary_path, "w") as f:
         json.dump(summ, f, indent=1, sort_keys=True)
@@ -182,8 +218,16 @@ def cmd_ga(args) -> int:
     _check_writable(args.out)
     base = E.GAConfig(pop_size=args.pop, length=args.length, mode=args.mode, cutoff=args.cutoff,
                       target=args.target, stop_when=args.stop_when)
-    rows = E.sweep(grid, runs=args.runs, base=base, seed0=args.seed, sample_size=args.sample_size,
-                   resamples=args.bootstrap, out=args.out)
+    rank, world = _dist()
+    if world > 1:
+        from .distributed import sweep_distributed
+        rows = sweep_distributed(grid, runs=args.runs, base=base, seed0=args.seed, sample_size=args.sample_size,
+                                 resamples=args.bootstrap, out=args.out)
+        if rank != 0:
+            return 0
+    else:
+        rows = E.sweep(grid, runs=args.runs, base=base, seed0=args.seed, sample_size=args.sample_size,
+                       resamples=args.bootstrap, out=args.out)
     _write_echo(_echo_path(args, args.out), "ga", args)
     if not args.quiet:
         for r in rows:
@@ -355,7 +399,8 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--hist-k", type=int, help="k the histogram attributes at (default: max ks)")
     p.add_argument("--workers", type=int, default=None, help="accepted for compatibility; the device schedules")
     p.add_argument("--batch-size", type=int, default=1 << 26)
-    p.add_argument("--start", type=int, default=0)
+    # (--start-index: torchrun's own parser rejects "--start" as an abbreviation of --start-method)
+    p.add_argument("--start-index", "--start", dest="start", type=int, default=0)
     p.add_argument("--count", type=int, default=None)
     p.add_argument("--out", help="histogram CSV path (required)")
     p.add_argument("--summary", help="summary JSON path (default <out>.summary.json)")
@@ -426,6 +471,11 @@ def main(argv=None) -> int:
     except CliError as e:
         print(f"tilevolve {args.command}: error: {e}", file=sys.stderr)
         return 2
+    finally:
+        if "torch.distributed" in sys.modules:
+            import torch.distributed as dist
+            if dist.is_available() and dist.is_initialized():
+                dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -171,6 +171,37 @@ def allreduce_device_histogram(dev: DeviceHistogram, group=None, meta: dict | No
     return gather_sharded(part, group)
 
 
+def sweep_distributed(mu_L_grid, runs: int = 100, base=None, seed0: int = 0, sample_size: int = 100,
+                      resamples: int = 10000, out: str | None = None, group=None, runner=None) -> list[dict]:
+    """evolve.sweep over all ranks of ``group`` (GA: replicas only).  Run r of
+    every sweep point goes to rank r mod R, each rank launches its runs of a point at once
+    (evolve.sweep_runs: one replica launch), and one all_gather_object brings every run's
+    discovery / adaptation time to every rank.  Run r uses seed seed0 + r wherever it runs,
+    so the rows equal evolve.sweep's exactly; rank 0 writes ``out``."""
+    import torch.distributed as dist
+    from .evolve import GAConfig, sweep_row, sweep_runs, write_sweep_json
+    runner = runner or sweep_runs
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    base = base or GAConfig()
+    cfgs = [GAConfig(**{**base.__dict__, "mu_L": float(mu)}) for mu in mu_L_grid]
+    mine = []
+    for i, cfg in enumerate(cfgs):
+        seeds = [seed0 + r for r in range(rank, runs, world)]
+        recs = runner(cfg, seeds) if seeds else []
+        mine.append([(s, rec.discovery, rec.adaptation) for s, rec in zip(seeds, recs)])
+    parts = [None] * world
+    dist.all_gather_object(parts, mine, group=group)
+    rows = []
+    for i, (mu, cfg) in enumerate(zip(mu_L_grid, cfgs)):
+        got = sorted((t for p in parts for t in p[i]), key=lambda t: t[0])
+        if [t[0] for t in got] != [seed0 + r for r in range(runs)]:
+            raise RuntimeError("sweep_distributed: runs missing after the gather")
+        rows.append(sweep_row(mu, cfg, [t[1] for t in got], [t[2] for t in got], sample_size, resamples))
+    if out is not None and rank == 0:
+        write_sweep_json(out, rows, base, seed0=seed0, sample_size=sample_size, resamples=resamples)
+    return rows
+
+
 def rank_chunks(plan: list, rank: int, world: int) -> list:
     """Round-robin assignment of enumeration chunks to ranks."""
     return [c for i, c in enumerate(plan) if i % world == rank]

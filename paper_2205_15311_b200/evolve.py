@@ -448,23 +448,36 @@ def censored_median_ci(vals, cutoff: int, sample_size: int = 100, resamples: int
                 ci_lo_censored=bool(cens and lo >= cutoff), ci_hi_censored=bool(cens and hi >= cutoff))
 
 
+def sweep_runs(cfg: GAConfig, seeds) -> list[RunRecord]:
+    """The runs of one sweep point: one replica launch when the population fits shared
+    memory, else one run_ga per seed."""
+    seeds = [int(x) for x in seeds]
+    return run_replicas(cfg, seeds) if cfg.pop_size <= REPLICA_MAX_POP else [run_ga(cfg, seed=x) for x in seeds]
+
+
+def sweep_row(mu: float, cfg: GAConfig, discovery: list, adaptation: list, sample_size: int = 100,
+              resamples: int = 10000) -> dict:
+    """One SPEC:452 sweep row from the per-run times (run order = seed order)."""
+    return {"muL": float(mu), "runs": len(discovery),
+            "discovery": censored_median_ci(discovery, cfg.cutoff, sample_size, resamples),
+            "adaptation": censored_median_ci(adaptation, cfg.cutoff, sample_size, resamples)}
+
+
 def sweep(mu_L_grid, runs: int = 100, base: GAConfig | None = None, seed0: int = 0, sample_size: int = 100,
-          resamples: int = 10000, out: str | None = None) -> list[dict]:
+          resamples: int = 10000, out: str | None = None, runner=sweep_runs) -> list[dict]:
     """SPEC:452 sweep rows: {muL, runs, discovery:{median, ci_lo, ci_hi, censored}, adaptation:{...}}.
 
-    Censoring follows SPEC:448 (``censored_median_ci``).  With ``out`` the rows are
-    written as the sweep JSON artefact, together with the configuration."""
+    Run r of every point uses seed seed0 + r.  Censoring follows SPEC:448
+    (``censored_median_ci``).  With ``out`` the rows are written as the sweep JSON
+    artefact, together with the configuration.  ``distributed.sweep_distributed``
+    deals the runs over GPUs and returns the same rows."""
     base = base or GAConfig()
     rows = []
     for mu in mu_L_grid:
         cfg = GAConfig(**{**base.__dict__, "mu_L": float(mu)})
-        seeds = [seed0 + r for r in range(runs)]
-        recs = (run_replicas(cfg, seeds) if cfg.pop_size <= REPLICA_MAX_POP
-                else [run_ga(cfg, seed=x) for x in seeds])
-        row = {"muL": float(mu), "runs": runs}
-        for name, vals in (("discovery", [r.discovery for r in recs]), ("adaptation", [r.adaptation for r in recs])):
-            row[name] = censored_median_ci(vals, cfg.cutoff, sample_size, resamples)
-        rows.append(row)
+        recs = runner(cfg, [seed0 + r for r in range(runs)])
+        rows.append(sweep_row(mu, cfg, [r.discovery for r in recs], [r.adaptation for r in recs], sample_size,
+                              resamples))
     if out is not None:
         write_sweep_json(out, rows, base, seed0=seed0, sample_size=sample_size, resamples=resamples)
     return rows

@@ -153,3 +153,53 @@ def test_allreduce_payload_from_representative_rank():
     res = _spawn(_collision_worker, 2)
     for r in res:
         assert r[1:] == (7, 1, 3, 3, 7), r
+
+
+# ---------------------------------------------------------------- GA sweeps over ranks (replicas only)
+class _FakeRun:
+    def __init__(self, discovery, adaptation):
+        self.discovery, self.adaptation = discovery, adaptation
+
+
+def _fake_runner(cfg, seeds):
+    """Deterministic stand-in for evolve.sweep_runs (no GPU here): per-run times as a function
+    of (muL, seed), censored (None) often enough to exercise both SPEC:448 branches."""
+    out = []
+    for s in seeds:
+        r = np.random.default_rng(int(s) * 7919 + int(round(cfg.mu_L * 1000)))
+        p = 0.2 if cfg.mu_L < 1 else 0.7
+        d = None if r.random() < p else int(r.integers(1, cfg.cutoff))
+        a = None if (d is None or r.random() < p) else int(r.integers(d, cfg.cutoff))
+        out.append(_FakeRun(d, a))
+    return out
+
+
+def _sweep_worker(rank, world, port, out_dir, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    from paper_2205_15311_b200 import evolve as E
+    from paper_2205_15311_b200.distributed import sweep_distributed
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        grid, runs = [0.1, 0.3, 4.0], 37
+        base = E.GAConfig(cutoff=500)
+        out = os.path.join(out_dir, "sweep.json")
+        rows = sweep_distributed(grid, runs, base, seed0=11, sample_size=40, resamples=500, out=out,
+                                 runner=_fake_runner)
+        ref = E.sweep(grid, runs, base, seed0=11, sample_size=40, resamples=500, runner=_fake_runner)
+        dist.barrier()
+        q.put((rank, rows == ref, os.path.exists(out), [r["adaptation"]["median"] is None for r in rows]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sweep_distributed_equals_sweep(world, tmp_path):
+    """Run r of every point on rank r mod R, one all_gather_object: the rows equal the
+    single-process sweep exactly (same seeds, same bootstrap), on every rank."""
+    res = _spawn(_sweep_worker, world, str(tmp_path))
+    assert sorted(r[0] for r in res) == list(range(world))
+    assert all(r[1] for r in res), res
+    assert all(r[2] for r in res)  # rank 0 wrote the sweep JSON
+    assert res[0][3][-1] is True and res[0][3][0] is False  # both censoring branches occur
