@@ -22,6 +22,10 @@
 //      CTA total (the prologue does the same for the initial population);
 //   -- grid barrier --
 // Two grid barriers per generation.
+// Staged mode (popcount fitness, L <= 32, CTA chunk within 200 KB of shared memory): between
+// the phases a CTA keeps its chunk's genomes, fitness and row offsets in shared memory, so
+// phase B reads nothing from L2 and phase C stores only row statistics; guide entries then
+// also carry genome j + 1 (a draw past the owner's range is resolved from the same entry).
 // Data written by other CTAs is read only after a grid barrier (grid.sync()
 // orders and publishes all prior writes of the grid; its gpu-scope acquire
 // invalidates L1), so ordinary cached loads are used.
