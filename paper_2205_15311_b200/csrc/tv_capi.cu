@@ -402,15 +402,12 @@ bool same_enumeration(const ClassifyParams &a, const ClassifyParams &b) {
 
 // Fill the payload of every slot whose payload is not its representative's
 // (tv_hist.cuh): replay those representatives' runs until one reproduces the key.
-int fix_payloads(tv_hist *h, cudaStream_t st) {
+int fix_payloads(tv_hist *h, cudaStream_t st, int64_t nkeys) {  // nkeys: tv_hist_count's, just read
   const HistDev &H = h->H;
   Scratch S(st);
   unsigned int *cnt;
   uint32_t *slots;
   unsigned long long *idx;
-  unsigned int nkeys = 0;
-  CK(cudaMemcpyAsync(&nkeys, H.n_keys, 4, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
   if (nkeys == 0) return 0;
   uint32_t *keys;
   CK(S.get(&cnt, 2)); CK(S.get(&slots, nkeys)); CK(S.get(&idx, nkeys)); CK(S.get(&keys, nkeys));
@@ -692,6 +689,14 @@ int tv_hist_destroy(tv_hist *h) {
   return 0;
 }
 
+namespace {
+// Page-locked staging for histogram exports, one per process (grown on demand, never freed:
+// a page-locked allocation costs milliseconds, so it is paid once, not per histogram).
+std::mutex g_pinned_mu;
+void *g_pinned = nullptr;
+size_t g_pinned_bytes = 0;
+}  // namespace
+
 int tv_hist_clear(tv_hist *h, void *stream) {
   if (!h) return fail(TV_ERR_ARG, "null histogram");
   h->has_params = false;
@@ -722,9 +727,66 @@ int tv_hist_export(tv_hist *h, int64_t max_records, uint32_t *keys, uint64_t *de
   int32_t ovf = 0;
   if (int rc = tv_hist_count(h, &n, &ovf, stream)) return rc;
   if (ovf) return fail(TV_ERR_HIST_FULL, "histogram overflowed its %lld slots", (long long)h->H.cap);
-  if (int rc = fix_payloads(h, st)) return rc;
+  if (int rc = fix_payloads(h, st, n)) return rc;
   if (n > max_records) return fail(TV_ERR_ARG, "%lld records do not fit max_records=%lld", (long long)n, (long long)max_records);
   const HistDev &H = h->H;
+  // host outputs (the documented case): every column is gathered into one device block and
+  // comes back in ONE copy through page-locked staging (ten pageable copies cost ~0.3 ms)
+  const void *outs[10] = {keys, det, steric, rep_det, rep_any, w, hh, cells, shape, tallies};
+  bool all_host = true;
+  for (const void *o : outs) all_host = all_host && (!o || !is_device_ptr(o));
+  if (all_host) {
+    const size_t sz[10] = {(size_t)n * 4, (size_t)n * 8, (size_t)n * 8, (size_t)n * 8, (size_t)n * 8, (size_t)n,
+                           (size_t)n, (size_t)n * 2, (size_t)n * H.W * 8, (size_t)H.q * 5 * 8};
+    size_t off[10], total = 0;
+    for (int i = 0; i < 10; i++) { off[i] = total; total += (sz[i] + 15) / 16 * 16; }
+    std::lock_guard<std::mutex> lock(g_pinned_mu);
+    if (g_pinned_bytes < total) {
+      if (g_pinned) cudaFreeHost(g_pinned);
+      g_pinned = nullptr;
+      g_pinned_bytes = 0;
+      CK(cudaHostAlloc(&g_pinned, std::max<size_t>(total, 1 << 20), cudaHostAllocDefault));
+      g_pinned_bytes = std::max<size_t>(total, 1 << 20);
+    }
+    {
+      Scratch S(st);
+      char *blk;
+      uint32_t *k0, *s0, *s1;
+      unsigned int *cnt;
+      CK(S.get(&blk, total)); CK(S.get(&k0, std::max<int64_t>(n, 1))); CK(S.get(&s0, std::max<int64_t>(n, 1)));
+      CK(S.get(&s1, std::max<int64_t>(n, 1))); CK(S.get(&cnt, 1));
+      HistRecords R;
+      R.keys = reinterpret_cast<uint32_t *>(blk + off[0]);
+      R.det = reinterpret_cast<unsigned long long *>(blk + off[1]);
+      R.steric = reinterpret_cast<unsigned long long *>(blk + off[2]);
+      R.rep_det = reinterpret_cast<unsigned long long *>(blk + off[3]);
+      R.rep_any = reinterpret_cast<unsigned long long *>(blk + off[4]);
+      R.w = reinterpret_cast<uint8_t *>(blk + off[5]);
+      R.h = reinterpret_cast<uint8_t *>(blk + off[6]);
+      R.cells = reinterpret_cast<uint16_t *>(blk + off[7]);
+      R.shape = reinterpret_cast<unsigned long long *>(blk + off[8]);
+      CK(cudaMemsetAsync(cnt, 0, 4, st));
+      k_hist_compact<<<256, 256, 0, st>>>(H, k0, s0, cnt);
+      CK(cudaGetLastError());
+      if (n > 0) {
+        size_t tmp_bytes = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k0, R.keys, s0, s1, (int)n, 0, 32, st));
+        uint8_t *tmp;
+        CK(S.get(&tmp, tmp_bytes));
+        CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k0, R.keys, s0, s1, (int)n, 0, 32, st));
+        k_hist_gather<<<64, 256, 0, st>>>(H, s1, n, R);
+        CK(cudaGetLastError());
+      }
+      CK(cudaMemcpyAsync(blk + off[9], H.tallies, sz[9], cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(g_pinned, blk, total, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    void *dst[10] = {keys, det, steric, rep_det, rep_any, w, hh, cells, shape, tallies};
+    for (int i = 0; i < 10; i++)
+      if (dst[i] && sz[i]) memcpy(dst[i], static_cast<char *>(g_pinned) + off[i], sz[i]);
+    if (n_out) *n_out = n;
+    return 0;
+  }
   {
     Scratch S(st);
     uint32_t *k0, *s0, *k1, *s1;
