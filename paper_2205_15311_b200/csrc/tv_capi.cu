@@ -766,6 +766,7 @@ int tv_hist_export(tv_hist *h, int64_t max_records, uint32_t *keys, uint64_t *de
       R.cells = reinterpret_cast<uint16_t *>(blk + off[7]);
       R.shape = reinterpret_cast<unsigned long long *>(blk + off[8]);
       CK(cudaMemsetAsync(cnt, 0, 4, st));
+      CK(cudaMemsetAsync(blk, 0, total, st));  // (the alignment padding travels with the one copy)
       k_hist_compact<<<256, 256, 0, st>>>(H, k0, s0, cnt);
       CK(cudaGetLastError());
       if (n > 0) {
