@@ -627,6 +627,53 @@ def test_jatam_fitness_memo_is_exact(monkeypatch):
 
 
 @pytest.mark.gpu
+def test_jatam_fitness_generic_kernel_with_memo(monkeypatch):
+    """JaTAM fitness in a space the bitboard kernel does not take (b = 16 labels: the generic
+    thread-per-genome kernel, which inserts into the memo; lookups belong to the bitboard path's
+    pre-pass), memo forced on: a first and a repeated call on the same population both equal the
+    oracle."""
+    from paper_2205_15311_b200._kernels import edges_from_labels
+    from paper_2205_15311_b200.genome import SearchSpace, decode_tileset, genome_at_index
+    monkeypatch.setenv("TV_FITMEMO", "1")
+    sp = SearchSpace(2, 16)
+    d, k, n = 13, 4, 600
+    rng = np.random.default_rng(21)
+    grid = np.empty(d * d, np.int16)
+
+    def edges(idx):
+        ts = decode_tileset(genome_at_index(sp, idx), sp)
+        return edges_from_labels(np.array([v for t in ts.tiles for v in t], np.uint8), 2)
+
+    def expected(idx, target):
+        sw = np.zeros(4, np.uint64)
+        st, cls, *_ = O.classify_single(edges(idx), 2, d, k, 0, idx, True, sw)
+        if st != 0 or cls != 0:
+            return 0
+        O.assemble_single(edges(idx), 2, d, 0, idx, 0, True, grid)
+        return d * d - int(np.count_nonzero((grid >= 0).reshape(d, d) != target))
+
+    pool = rng.integers(0, 1 << 32, 150, dtype=np.uint64)
+    target = None
+    for idx in pool:  # a DET target shape from the pool
+        sw = np.zeros(4, np.uint64)
+        st, cls, *_ = O.classify_single(edges(int(idx)), 2, d, k, 0, int(idx), True, sw)
+        if st == 0 and cls == 0:
+            O.assemble_single(edges(int(idx)), 2, d, 0, int(idx), 0, True, grid)
+            target = (grid >= 0).reshape(d, d).copy()
+            break
+    assert target is not None
+    ga = E.DeviceGA(n, 32, 0.5, "asexual")
+    exp = {int(x): expected(int(x), target) for x in pool}
+    pop = pool[rng.integers(0, pool.size, n)]
+    ga.set_population(pop)
+    for rep in range(2):
+        f = ga.jatam_fitness(sp, target, d, k).cpu().numpy().view(np.uint32)
+        assert [int(v) for v in f] == [exp[int(x)] for x in pop], rep
+    assert any(exp.values())  # some genomes are DET (non-zero fitness)
+    ga.close()
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("n", [3000, 8192])
 def test_run_jatam_equals_generation_by_generation(n):
     """tv_ga_run_jatam (all generations enqueued at once) == jatam_fitness + run(f_ext) per generation:
