@@ -231,3 +231,23 @@ def test_render_atlas_from_histogram(tmp_path, capsys):
         bm = np.array([[c == "#" for c in ln] for ln in lines[2:]], bool)
         s = CroppedShape(bm.shape[1], bm.shape[0], bm)
         assert f"0x{shape_hash(s):08x}" == r["hash_hex"]  # the drawn shape is the CSV row's shape
+
+
+def test_torchrun_refuses_checkpoint_options(tmp_path):
+    """Under torchrun (two CPU ranks over gloo) a multi-GPU enumeration is one pass: --checkpoint
+    is refused on every rank with the CLI's one-line error, before any device work."""
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TV_DIST_BACKEND="gloo", CUDA_VISIBLE_DEVICES="")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), "-m", "paper_2205_15311_b200",
+                        "enumerate", "--tiles", "2", "--labels", "4", "--out", str(tmp_path / "x.csv"),
+                        "--checkpoint", str(tmp_path / "ck.bin")], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode != 0
+    assert r.stderr.count("--checkpoint / --resume are single-GPU options") == 2
