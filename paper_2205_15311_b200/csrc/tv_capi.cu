@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -1248,10 +1249,13 @@ int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **
     P.stg = L <= 32 && bytes <= (size_t)200 * 1024 && (es ? atoi(es) != 0 : true);
     P.pair = ep ? atoi(ep) != 0 : 1;
     h->smem = P.stg ? bytes : 0;
-    static bool attr = false;  // once per process, at the cap (handles differ in chunk size)
-    if (P.stg && !attr) {
+    // once per device, at the cap (handles differ in chunk size)
+    static std::atomic<unsigned long long> attr_set{0};
+    if (P.stg && dev < 64 && !((attr_set.load() >> dev) & 1ULL)) {
       CK(cudaFuncSetAttribute(k_ga_run, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr = true;
+      attr_set.fetch_or(1ULL << dev);
+    } else if (P.stg && dev >= 64) {
+      CK(cudaFuncSetAttribute(k_ga_run, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     }
   }
   int per_sm = 0;
@@ -1298,6 +1302,14 @@ int tv_ga_create(int64_t n, int32_t L, int32_t mode, const uint64_t *T, tv_ga **
     for (int a = 0; a < K && e == cudaSuccess; a++) {
       if (a && gap_bytes) e = cudaMalloc(&gap[a], gap_bytes);
       e = e ? e : cudaMalloc(&arena[a], total);
+      if (e != cudaSuccess && a > 0) {  // out of memory for more candidates: calibrate what there is
+        cudaGetLastError();
+        e = cudaSuccess;
+        if (gap[a]) cudaFree(gap[a]);
+        gap[a] = arena[a] = nullptr;
+        K = a;
+        break;
+      }
       if (e != cudaSuccess || K == 1) break;
       bind(arena[a]);
       GaParams Q = P;
