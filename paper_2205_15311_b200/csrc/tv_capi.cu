@@ -83,6 +83,15 @@ struct Scratch {
   }
 };
 
+// A handle's buffers live on the device it was created on: calls with another device current
+// would launch there on foreign memory, so they fail loudly instead.
+int on_device(int want) {
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess) return fail(TV_ERR_CUDA, "no CUDA device");
+  if (cur != want) return fail(TV_ERR_ARG, "handle belongs to device %d, the current device is %d", want, cur);
+  return 0;
+}
+
 int current_device(int *dev) {
   cudaError_t e = cudaGetDevice(dev);
   if (e != cudaSuccess) return fail(TV_ERR_CUDA, "no CUDA device: %s", cudaGetErrorString(e));
@@ -700,6 +709,7 @@ size_t g_pinned_bytes = 0;
 
 int tv_hist_clear(tv_hist *h, void *stream) {
   if (!h) return fail(TV_ERR_ARG, "null histogram");
+  if (int rc = on_device(h->device)) return rc;
   h->has_params = false;
   k_hist_reset<<<256, 256, 0, (cudaStream_t)stream>>>(h->H);
   CK(cudaGetLastError());
@@ -708,6 +718,7 @@ int tv_hist_clear(tv_hist *h, void *stream) {
 
 int tv_hist_count(tv_hist *h, int64_t *n_keys, int32_t *overflow, void *stream) {
   if (!h) return fail(TV_ERR_ARG, "null histogram");
+  if (int rc = on_device(h->device)) return rc;
   unsigned int v[2];
   cudaStream_t st = (cudaStream_t)stream;
   CK(cudaMemcpyAsync(&v[0], h->H.n_keys, 4, cudaMemcpyDeviceToHost, st));
@@ -723,6 +734,7 @@ int tv_hist_export(tv_hist *h, int64_t max_records, uint32_t *keys, uint64_t *de
                    int64_t *tallies, int64_t *n_out, void *stream) {
   NvtxRange nvtx_("tv_hist_export");
   if (!h) return fail(TV_ERR_ARG, "null histogram");
+  if (int rc = on_device(h->device)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   int64_t n = 0;
   int32_t ovf = 0;
@@ -830,6 +842,7 @@ int tv_hist_pack(tv_hist *h, int64_t max_records, uint64_t *rows, int64_t *talli
                  void *stream) {
   NvtxRange nvtx_("tv_hist_pack");
   if (!h) return fail(TV_ERR_ARG, "null histogram");
+  if (int rc = on_device(h->device)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   int64_t n = 0;
   int32_t ovf = 0;
@@ -869,6 +882,7 @@ int tv_hist_pack(tv_hist *h, int64_t max_records, uint64_t *rows, int64_t *talli
 int tv_hist_replace_rows(tv_hist *h, int64_t n, const uint64_t *rows, const int64_t *tallies, void *stream) {
   NvtxRange nvtx_("tv_hist_replace_rows", (long long)n);
   if (!h) return fail(TV_ERR_ARG, "null histogram");
+  if (int rc = on_device(h->device)) return rc;
   if (n < 0) return fail(TV_ERR_ARG, "negative n");
   cudaStream_t st = (cudaStream_t)stream;
   HistDev &H = h->H;
@@ -910,6 +924,7 @@ int tv_hist_merge(tv_hist *h, int64_t n, const uint32_t *keys, const uint64_t *d
                   const uint64_t *rep_det, const uint64_t *rep_any, const uint8_t *w, const uint8_t *hh,
                   const uint16_t *cells, const uint64_t *shape, const int64_t *tallies, void *stream) {
   if (!h) return fail(TV_ERR_ARG, "null histogram");
+  if (int rc = on_device(h->device)) return rc;
   if (n < 0) return fail(TV_ERR_ARG, "negative n");
   cudaStream_t st = (cudaStream_t)stream;
   const HistDev &H = h->H;
@@ -955,6 +970,7 @@ static int enumerate_common(const uint64_t *indices, uint64_t start, uint64_t ch
                             int32_t strict, tv_hist *h, void *stream) {
   NvtxRange nvtx_("tv_enumerate", (long long)count);
   if (!h) return fail(TV_ERR_ARG, "null histogram");
+  if (int rc = on_device(h->device)) return rc;
   if (count < 0) return fail(TV_ERR_ARG, "negative count");
   Common C;
   if (int rc = fill_common(a, bpl, mask_pos, mask_val, m, free_pos, nfree, d, ks, q, hist_k, seed, strict, C)) return rc;
@@ -1388,6 +1404,7 @@ int tv_ga_destroy(tv_ga *h) {
 
 int tv_ga_set_population(tv_ga *h, const uint64_t *genomes, void *stream) {
   if (!h) return fail(TV_ERR_ARG, "null GA");
+  if (int rc = on_device(h->device)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   h->fknown_valid = false;
   h->memo_clear = true;  // a new run: the fitness memo starts empty (a repeated run is re-classified)
@@ -1412,6 +1429,7 @@ int tv_ga_set_population(tv_ga *h, const uint64_t *genomes, void *stream) {
 
 int tv_ga_get_population(tv_ga *h, uint64_t *out, void *stream) {
   if (!h) return fail(TV_ERR_ARG, "null GA");
+  if (int rc = on_device(h->device)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   const unsigned long long *src = h->cur ? h->P.pop1 : h->P.pop0;
   if (h->W == 1) {
@@ -1441,6 +1459,7 @@ int tv_ga_run(tv_ga *h, uint64_t seed, int64_t g0, int64_t n_gens, uint32_t targ
               int64_t *gens_done, void *stream) {
   NvtxRange nvtx_("tv_ga_run", (long long)n_gens);
   if (!h) return fail(TV_ERR_ARG, "null GA");
+  if (int rc = on_device(h->device)) return rc;
   if (n_gens < 1) return fail(TV_ERR_ARG, "n_gens must be >= 1");
   if (f_ext && n_gens != 1) return fail(TV_ERR_ARG, "an external fitness vector covers exactly one generation");
   if (f_ext && !is_device_ptr(f_ext)) return fail(TV_ERR_ARG, "external fitness must be a device pointer");
@@ -1621,6 +1640,7 @@ int tv_ga_fitness_jatam(tv_ga *h, int32_t a, int32_t bpl, const int64_t *mask_po
                         int32_t strict, const uint8_t *target_occ, uint32_t *f_out, void *stream) {
   NvtxRange nvtx_("tv_ga_fitness_jatam");
   if (!h) return fail(TV_ERR_ARG, "null GA");
+  if (int rc = on_device(h->device)) return rc;
   if (h->W > 1) return fail(TV_ERR_ARG, "JaTAM fitness needs L <= 64");
   if (d > 29) return fail(TV_ERR_ARG, "JaTAM fitness supports d <= 29");
   if (nfree != h->P.L) return fail(TV_ERR_ARG, "GA genome length %d != %lld free bits", h->P.L, (long long)nfree);
@@ -1656,6 +1676,7 @@ int tv_ga_run_jatam(tv_ga *h, int32_t a, int32_t bpl, const int64_t *mask_pos, c
                     uint32_t *best, uint64_t *sum, uint32_t *count, void *stream) {
   NvtxRange nvtx_("tv_ga_run_jatam", (long long)n_gens);
   if (!h) return fail(TV_ERR_ARG, "null GA");
+  if (int rc = on_device(h->device)) return rc;
   if (h->W > 1) return fail(TV_ERR_ARG, "JaTAM fitness needs L <= 64");
   if (n_gens < 1) return fail(TV_ERR_ARG, "n_gens must be >= 1");
   if (d > 29) return fail(TV_ERR_ARG, "JaTAM fitness supports d <= 29");

@@ -227,6 +227,7 @@ class DeviceGA:
         _lib.check(_lib.lib().tv_ga_create(self.n, self.L, self.mode, _lib.ptr(self.T), ctypes.byref(h)))
         self._h = h
         self._fit = None
+        self.device = _current_device()  # the handle's buffers live there (the C ABI checks it)
 
     def close(self):
         if self._h:
@@ -316,12 +317,17 @@ _GA_POOL: "collections.OrderedDict" = None
 _GA_POOL_MAX = 4
 
 
+def _current_device() -> int:
+    import torch
+    return torch.cuda.current_device() if torch.cuda.is_available() else -1
+
+
 def _ga_acquire(n: int, L: int, mu_L: float, mode) -> "DeviceGA":
     import collections
     global _GA_POOL
     if _GA_POOL is None:
         _GA_POOL = collections.OrderedDict()
-    key = (int(n), int(L), float(mu_L), mode)
+    key = (_current_device(), int(n), int(L), float(mu_L), mode)
     ga = _GA_POOL.pop(key, None)
     if ga is None or not ga._h:
         return DeviceGA(n, L, mu_L, mode)
@@ -330,7 +336,7 @@ def _ga_acquire(n: int, L: int, mu_L: float, mode) -> "DeviceGA":
 
 
 def _ga_release(ga: "DeviceGA", mu_L: float, mode) -> None:
-    key = (ga.n, ga.L, float(mu_L), mode)
+    key = (ga.device, ga.n, ga.L, float(mu_L), mode)
     old = _GA_POOL.pop(key, None)
     if old is not None:
         old.close()

@@ -704,3 +704,17 @@ def test_run_jatam_equals_generation_by_generation(n):
                               init=init), fitness=E.JatamFitness(S28, target), seed=13)
     assert np.array_equal(rec.best, b1) and np.array_equal(rec.count_at_target, c1)
     g1.close(); g2.close()
+
+
+@pytest.mark.gpu
+def test_handles_refuse_another_device():
+    """A GA / histogram handle used while another device is current fails loudly (its buffers
+    live on the device it was created on).  Needs two GPUs; skipped otherwise."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("one GPU")
+    ga = E.DeviceGA(1000, 24, 0.3)
+    with torch.cuda.device(1):
+        with pytest.raises(ValueError, match="belongs to device 0"):
+            ga.run(1, 0, 3, 10, 1000, 0)
+    ga.close()
