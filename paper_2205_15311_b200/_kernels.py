@@ -79,11 +79,12 @@ def classify_batch(indices, a, bpl, mask_pos, mask_val, free_pos, d, ks, hist_k,
     if len(out_shape.shape) != 2:
         raise ValueError("out_shape must be (n, W)")
     W = int(out_shape.shape[1])
-    stream = _lib.stream_of(idx, *outs)
-    _lib.check(L.tv_classify_batch(
-        _lib.ptr(idx), n, int(a), int(bpl), _lib.ptr(mp), _lib.ptr(mv), mp.shape[0], _lib.ptr(fp), fp.shape[0],
-        int(d), _lib.ptr(ksa), q, int(hist_k), int(np.uint64(seed)), int(bool(strict)),
-        *[_lib.ptr(o) for o in outs], W, stream))
+    with _lib.device_of(idx, *outs):  # device tensors: run on their device, on its current stream
+        stream = _lib.stream_of(idx, *outs)
+        _lib.check(L.tv_classify_batch(
+            _lib.ptr(idx), n, int(a), int(bpl), _lib.ptr(mp), _lib.ptr(mv), mp.shape[0], _lib.ptr(fp), fp.shape[0],
+            int(d), _lib.ptr(ksa), q, int(hist_k), int(np.uint64(seed)), int(bool(strict)),
+            *[_lib.ptr(o) for o in outs], W, stream))
 
 
 def assemble_single(edges, a, d, seed, genome_index, run_index, strict, out_grid):

@@ -138,6 +138,19 @@ def stream_of(*arrays):
     return None
 
 
+def device_of(*arrays):
+    """Context that makes the CUDA tensors' device current for a call (a no-op for host
+    arrays); tensors on different devices are refused."""
+    import contextlib
+    devs = {a.device.index for a in arrays if is_cuda(a)}
+    if not devs:
+        return contextlib.nullcontext()
+    if len(devs) > 1:
+        raise ValueError(f"CUDA tensors on different devices {sorted(devs)}")
+    import torch
+    return torch.cuda.device(devs.pop())
+
+
 def launch_info() -> dict:
     info = (ctypes.c_int64 * 5)()
     lib().tv_last_launch_info(info)
