@@ -369,12 +369,13 @@ def s32_bench(args, rank: int, world: int, stream, peak: float | None = None) ->
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    run(mine * chunk)
-    if world > 1:  # the merged histogram stays on the GPUs, sharded by key
-        allreduce_device_histogram(hist, None, export=False)
-    e1.record(stream)
-    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as cs:  # clocks over the ~5 s pass
+        e0.record(stream)
+        run(mine * chunk)
+        if world > 1:  # the merged histogram stays on the GPUs, sharded by key
+            allreduce_device_histogram(hist, None, export=False)
+        e1.record(stream)
+        torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     if world > 1:
         ms = max_over_ranks(ms)
@@ -410,11 +411,11 @@ def s32_bench(args, rank: int, world: int, stream, peak: float | None = None) ->
             "config": {"workload": "full S^32_(3,8) enumeration: 2^32 genomes -> phenotype histogram", "ks": [7],
                        "hist_k": 7, "d": 19, "seed": 0, "strict": True, "chunking": f"{chunk} round-robin",
                        "timed": "one pass after a 2^24 warm-up chunk (inputs are index ranges; no L2 reuse)"},
-            "histogram_ok": ok, "phenotypes": len(final), "cpu_baseline": cpu,
+            "histogram_ok": ok, "phenotypes": len(final), "cpu_baseline": cpu, "clocks": cs.summary(),
             "roofline": None if not peak else enum_roofline(
                 "k_classify_fast<3>", n_all / world, ms, peak, event_counts("s32_sample_2p22"),
-                "the whole timed pass: per 2^26-item slice k_prepass<3> + CUB radix sort + k_classify_fast<3> "
-                "(+ the exchange at N > 1); ops per genome from 64 evenly spaced 2^16 blocks")}
+                "the whole timed pass: per 2^26-item slice k_prepass<3> + the counting sort by key + "
+                "k_classify_fast<3> (+ the exchange at N > 1); ops per genome from 64 evenly spaced 2^16 blocks")}
 
 
 def ga_jatam_bench(n: int = 1 << 20, gens: int = 20, peak: float | None = None, cpu_leg: bool = True) -> dict:
