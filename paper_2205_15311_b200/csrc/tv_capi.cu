@@ -326,8 +326,25 @@ int launch_classify(Common &C, Scratch &S, cudaStream_t st) {
           P.order = want_order ? order : nullptr;
           P.n_skip = n_skip;
         }
+        unsigned long long *pt = nullptr;
+        const bool tail_prof = getenv("TV_TAIL_PROF") != nullptr;  // development aid
+        if (tail_prof) {
+          const unsigned long long init[3] = {~0ULL, ~0ULL, 0ULL};
+          CK(S.get(&pt, 3));
+          CK(cudaMemcpyAsync(pt, init, 24, cudaMemcpyHostToDevice, st));
+          CK(cudaStreamSynchronize(st));
+        }
+        P.prof_t = pt;
         void *args[] = {&P};
         CK(cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(threads), args, smem, st));
+        if (tail_prof) {
+          unsigned long long t[3];
+          CK(cudaMemcpyAsync(t, pt, 24, cudaMemcpyDeviceToHost, st));
+          CK(cudaStreamSynchronize(st));
+          fprintf(stderr, "k_classify_fast %lld items: %.3f ms, work queue empty after %.3f ms, drain %.3f ms\n",
+                  (long long)P.n, (t[2] - t[0]) / 1e6, (t[1] - t[0]) / 1e6, (t[2] - t[1]) / 1e6);
+        }
+        P.prof_t = nullptr;
       }
       P.n = n_all;
       P.item0 = 0;

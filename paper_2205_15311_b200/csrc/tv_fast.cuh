@@ -59,6 +59,12 @@ __device__ __forceinline__ int ffs_m(uint64_t x) {  // candidate flags never rea
   return lo ? __ffs(lo) - 1 : 31 + __ffs(hi);
 }
 
+__device__ __forceinline__ unsigned long long fast_clock() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 template <bool RING> struct FastLane {
   uint32_t *gw;     // &board word 0 of this lane (stride 32 words)
   uint16_t *sw;     // &movelist slot 0 of this lane: slot k at sw[k * 32] (lanes 2k, 2k+1 share a bank word)
@@ -424,6 +430,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
   bool tfree = false;  // no run of this genome can go TRIVIAL (k_prepass)
   Cand<A, STRICT> K;
 
+  if (P.prof_t && threadIdx.x == 0) atomicMin(&P.prof_t[0], fast_clock());
   // lanes not DONE (warp-uniform; lanes only finish in the refill below) and the parked-lane
   // count that triggers a service pass: min(thresh, half the live lanes), so never above nlive
   int nlive = 32, trig = min(thresh, 16);
@@ -638,6 +645,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
           item = (int64_t)base + __popc(need & ((1u << lane) - 1u));
           if (item >= n_run) {
             st = ST_DONE;
+            if (P.prof_t) atomicMin(&P.prof_t[1], fast_clock());
           } else {
             // behaviour-sorted processing order (k_prepass); every per-item output and flag below
             // is addressed by the item's own number, so the order is invisible to the caller
@@ -763,6 +771,7 @@ __global__ void __launch_bounds__(fast_threads<A>(), TV_FAST_MINB) k_classify_fa
     else if (sp == 0) pend = RUN_BOUNDED;
   }
 
+  if (P.prof_t) atomicMax(&P.prof_t[2], fast_clock());
   if (HIST) {
     __syncthreads();
     for (int s = threadIdx.x; s < HS; s += blockDim.x) {

@@ -63,6 +63,8 @@ struct ClassifyParams {
   const uint32_t *order;    // fast kernel, histogram mode: work-item permutation (k_prepass sort), or nullptr
   const unsigned long long *n_skip;  // fast kernel: the last *n_skip order entries (1-mers) are done, or nullptr
   unsigned long long *work; // dynamic work counter
+  unsigned long long *prof_t;  // optional (TV_TAIL_PROF): globaltimer at first CTA start, work queue
+                               // found empty, last CTA end (fast kernel)
   // generic kernel scratch (per thread, interleaved)
   int16_t *g_grid;
   uint8_t *g_mark;
